@@ -1,0 +1,191 @@
+/*
+ * pp200.h -- C ABI of the B200-native many-path homotopy tracker.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   template<class R> SolutionSet<R> track_all(const HomotopyInstance<R>&,
+ *       const StartData<R>&, const TrackConfig&, ProgressSink*, uint64_t lo, uint64_t hi)
+ *   (reference: proj/include/polypath/tracker.hpp:166-170, impl proj/src/tracker.cpp:511-540)
+ * and of the host calls that feed it (system parsing, homotopy construction, start data).
+ * Every entry point takes plain pointers and sizes; no C++ or torch types cross it.
+ *
+ * Precision is a runtime tag (reference: xprec.hpp:547 `enum class Precision {d, dd, qd}`).
+ * A value at precision R is stored as L = 1/2/4 binary64 limbs, most significant first;
+ * a complex value is [re limbs..., im limbs...] (2L doubles), the order of the reference's
+ * PlanarBlock planes (evaldiff.hpp:114-172).
+ *
+ * Errors: 0 = success; negative codes below.  PP_E_INVALID corresponds to the reference's
+ * std::invalid_argument (TrackConfig::validate, tracker.cpp:40-49; empty start set,
+ * tracker.cpp:516; dimension checks, homotopy.cpp:9-13).  PP_E_PARSE corresponds to
+ * polypath::ParseError (polysys.hpp:60-65); its line/column are in pp_last_error().
+ * Per-path failures are data (status/reason), never error codes (tracker.hpp:16-25).
+ * There is no CPU fallback: if no CUDA device is usable, device entry points return PP_E_CUDA.
+ */
+#ifndef PP200_H
+#define PP200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* precision tags (xprec.hpp:547) */
+enum { PP_D = 0, PP_DD = 1, PP_QD = 2 };
+
+/* error codes */
+enum {
+  PP_OK = 0,
+  PP_E_INVALID = -1,  /* std::invalid_argument in the reference */
+  PP_E_PARSE = -2,    /* polypath::ParseError */
+  PP_E_CUDA = -3,     /* CUDA runtime failure / no device */
+  PP_E_NOMEM = -4,
+  PP_E_CAPACITY = -5, /* caller buffer too small */
+  PP_E_DOMAIN = -6    /* std::domain_error (division by zero in xprec/complex) */
+};
+
+/* PathStatus (tracker.hpp:16) */
+enum { PP_FAILED = -1, PP_ACTIVE = 0, PP_SUCCESS = 1 };
+
+/* FailReason (tracker.hpp:18-25) */
+enum {
+  PP_REASON_NONE = 0,
+  PP_REASON_DIVERGED = 1,
+  PP_REASON_STEP_UNDERFLOW = 2,
+  PP_REASON_MAX_STEPS = 3,
+  PP_REASON_SINGULAR = 4,
+  PP_REASON_NO_CERTIFICATE = 5
+};
+
+/* TrackConfig (tracker.hpp:29-46); field meaning and defaults identical. */
+typedef struct pp_track_config {
+  double residual_tol;
+  double update_tol;
+  int32_t max_newton;
+  int32_t expand_after;
+  double h_init;
+  double h_min;
+  double h_max;
+  double expand;
+  double contract;
+  double divergence_bound;
+  uint32_t max_steps;
+  uint32_t batch;   /* reference cohort width; the device ignores it (persistent refill) */
+  uint32_t workers; /* reference CPU workers; the device ignores it */
+  uint32_t reserved;
+} pp_track_config;
+
+/*
+ * Output records: SolutionSet<R>::paths (tracker.hpp:73-94) as caller-owned SoA host buffers.
+ * Record i belongs to start index lo+i, so the set is sorted by path_id as in
+ * tracker.cpp:537-538.  x is [record][var][2L] doubles, residual is [record][L].
+ */
+typedef struct pp_records {
+  uint64_t capacity; /* records the buffers can hold (>= hi-lo) */
+  uint64_t count;    /* out: records written */
+  uint64_t* path_id;
+  int8_t* status;
+  uint8_t* reason;
+  uint32_t* steps;
+  uint32_t* newton_iters;
+  uint32_t* rejections;
+  double* x;
+  double* residual;
+} pp_records;
+
+/* Run statistics (SolutionSet::batches/total_rounds, tracker.hpp:89-94, plus device timing) */
+typedef struct pp_run_stats {
+  uint64_t paths;        /* terminal paths produced */
+  uint64_t batches;      /* device launches (the reference's cohorts) */
+  uint64_t total_rounds; /* loop trips of the slowest device slot */
+  uint64_t newton_iters; /* sum over paths, corrector iterations */
+  double device_ms;      /* tracking kernel time (CUDA events) */
+  double h2d_ms;         /* host->device staging */
+  double d2h_ms;         /* device->host record copy */
+  double wall_ms;        /* whole call */
+  uint64_t h2d_bytes;
+  uint64_t d2h_bytes;
+  uint32_t slots;        /* concurrent path slots on the device */
+  uint32_t kernel_launches;
+} pp_run_stats;
+
+typedef struct pp_system pp_system;     /* PolySystem (polysys.hpp:41-51) */
+typedef struct pp_starts pp_starts;     /* StartData<R> (homotopy.hpp:38-49) */
+typedef struct pp_homotopy pp_homotopy; /* HomotopyInstance<R> + device plan (homotopy.hpp:16-22) */
+
+const char* pp_version(void);
+/* message of the last failing call on this thread ("" if none) */
+const char* pp_last_error(void);
+/* number of binary64 limbs of a precision tag, 0 if the tag is invalid */
+int pp_limbs(int prec);
+
+/* ---- systems: polysys.hpp:67-79 (parse_system, print_system, cyclic_system, system_stats) ---- */
+int pp_system_parse(const char* text, size_t len, pp_system** out);
+int pp_system_cyclic(uint32_t n, pp_system** out);
+/* writes a NUL-terminated text form; *needed = bytes required including the NUL */
+int pp_system_print(const pp_system* s, char* buf, size_t cap, size_t* needed);
+int pp_system_stats(const pp_system* s, uint32_t* dim, uint32_t* n_polys, uint64_t* n_monomials,
+                    uint64_t* total_degree, int* total_degree_overflow);
+/* per-polynomial total degrees, n_polys entries */
+int pp_system_degrees(const pp_system* s, uint32_t* degrees);
+void pp_system_free(pp_system* s);
+
+/* ---- homotopy.hpp:24-68 ---- */
+/* random_gamma(seed) (homotopy.cpp:34-40) */
+void pp_random_gamma(uint64_t seed, double* re, double* im);
+/* total_degree_start<R>(f) (homotopy.cpp:87-113): start system g and lazily indexed starts */
+int pp_total_degree_start(const pp_system* f, int prec, pp_system** g_out, pp_starts** out);
+/* load_start_data<R>(g, parse_solutions(text), start_tol) (homotopy.cpp:115-140, polysys.cpp:381-425).
+ * The residual screening runs on the device.  Rejected candidates (0-based index and residual) are
+ * written to rejected_idx / rejected_resid up to rejected_cap entries; *n_rejected is the total. */
+int pp_load_start_data(const pp_system* g, int prec, const char* text, size_t len, double start_tol,
+                       int device, pp_starts** out, uint64_t* rejected_idx,
+                       double* rejected_resid, uint64_t rejected_cap, uint64_t* n_rejected);
+/* explicit start list, [count][dim][2L] doubles (StartProvenance::file) */
+int pp_starts_explicit(int prec, uint32_t dim, uint64_t count, const double* x, pp_starts** out);
+uint64_t pp_starts_count(const pp_starts* s);
+/* StartData::solution(index) (homotopy.cpp:73-85), dim×2L doubles */
+int pp_starts_solution(const pp_starts* s, uint64_t index, double* x);
+void pp_starts_free(pp_starts* s);
+
+/* make_homotopy<R>(f, g, gamma) (homotopy.cpp:7-20); gamma is 2L doubles (re limbs, im limbs) */
+int pp_make_homotopy(const pp_system* f, const pp_system* g, int prec, const double* gamma,
+                     pp_homotopy** out);
+/* plan geometry (EvalPlan, evaldiff.hpp:80-94) */
+int pp_homotopy_info(const pp_homotopy* h, uint32_t* dim, uint32_t* n_polys, uint32_t* n_terms,
+                     uint32_t* mon_rows, uint32_t* max_k, uint64_t* posprod_muls);
+void pp_homotopy_free(pp_homotopy* h);
+
+/* ---- tracker.hpp:29-46 ---- */
+void pp_track_config_defaults(int prec, pp_track_config* cfg); /* TrackConfig::defaults */
+int pp_track_config_validate(const pp_track_config* cfg);      /* TrackConfig::validate */
+
+/*
+ * track_all<R> (tracker.hpp:166-170): tracks starts [lo, min(count, hi)) on CUDA device `device`
+ * and writes one record per start into `out`.  Returns PP_E_INVALID for a bad config or an empty
+ * start set, exactly where the reference throws.  stats may be NULL.
+ */
+int pp_track_all(const pp_homotopy* h, const pp_starts* s, const pp_track_config* cfg,
+                 uint64_t lo, uint64_t hi, int device, pp_records* out, pp_run_stats* stats);
+
+/*
+ * eval_system_batch (evaldiff.hpp:228-230) on the device for `batch` points:
+ * points [batch][dim][2L], t [batch][L] -> sys [batch][n_polys][2L], jac [batch][n_polys*dim][2L]
+ * (row = poly*dim + var, evaldiff.hpp:181).  jac may be NULL.
+ */
+int pp_eval_batch(const pp_homotopy* h, uint32_t batch, const double* points, const double* t,
+                  double* sys, double* jac, int device);
+
+/*
+ * least_squares_solve (linalg.hpp:110-125) for `batch` independent n×n complex systems on the
+ * device: a [batch][col][row][2L] (column-major, as DenseMatrix), b [batch][n][2L] ->
+ * x [batch][n][2L]; ok[i] = 0 where the reference returns false (rank deficiency).
+ */
+int pp_lsq_batch(int prec, uint32_t n, uint32_t batch, const double* a, const double* b,
+                 double* x, uint8_t* ok, int device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PP200_H */

@@ -1,0 +1,34 @@
+/*
+ * pp200_testing.h -- test hooks exported by libpp200.so in addition to pp200.h.  Not part of the
+ * drop-in boundary; used by tests/ to compare the host arithmetic, decimal I/O and plan tables
+ * with the reference build bit for bit.
+ */
+#ifndef PP200_TESTING_H
+#define PP200_TESTING_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "pp200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* op: 0 add, 1 sub, 2 mul, 3 mul by double b[0], 4 div, 5 sqrt, 6 compare, 7 to_double,
+ * 8 complex mul, 9 complex div (Smith), 10 complex modulus.  Operands are limb arrays. */
+int pp_test_arith(int prec, int op, const double* a, const double* b, double* out);
+/* parse_decimal at a level (xprec_io.cpp:121-193) */
+int pp_test_parse_decimal(int prec, const char* s, double* out);
+/* to_decimal at a level (xprec_io.cpp:31-108, 198-212) */
+int pp_test_to_decimal(int prec, const double* in, char* buf, size_t cap);
+/* per-term (c_start, c_target) coefficient limbs of a homotopy's plan */
+int pp_test_plan_coeffs(const pp_homotopy* h, double* out, size_t cap);
+/* [mon_steps, cmul_steps, jac_terms, jac_scaled, n_base] of a homotopy's plan */
+int pp_homotopy_counts(const pp_homotopy* h, uint64_t* counts);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

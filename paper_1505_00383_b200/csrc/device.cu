@@ -1,0 +1,484 @@
+// device.cu -- host side of the CUDA path: plan upload, slot workspace, kernel selection and
+// launch, record download.  No computation of the path happens here.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "device.hpp"
+#include "kernels.hpp"
+
+namespace pp {
+
+namespace {
+
+void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaFailure(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+T* dmalloc(size_t count) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  check(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+  return static_cast<T*>(p);
+}
+
+template <class T>
+T* upload(const std::vector<T>& v) {
+  T* p = dmalloc<T>(v.size());
+  if (!v.empty()) check(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+  return p;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+      throw CudaFailure("no CUDA device available (the tracker has no CPU fallback)");
+    if (dev < 0 || dev >= count) throw CudaFailure("CUDA device index out of range");
+    check(cudaGetDevice(&prev), "cudaGetDevice");
+    check(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+const dev::Variant* pick_variant(int prec, uint32_t n, uint32_t max_k) {
+  int count = 0;
+  const dev::Variant* v = prec == 0 ? dev::variants_d(&count)
+                          : prec == 1 ? dev::variants_dd(&count)
+                                      : dev::variants_qd(&count);
+  const dev::Variant* best = nullptr;
+  for (int i = 0; i < count; ++i) {
+    if (v[i].nmax < static_cast<int>(n) || v[i].kmax < static_cast<int>(std::max<uint32_t>(max_k, 2))) continue;
+    if (best == nullptr || v[i].nmax < best->nmax || (v[i].nmax == best->nmax && v[i].kmax < best->kmax))
+      best = &v[i];
+  }
+  return best;
+}
+
+// grow-only per-device scratch arena
+struct Arena {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+std::mutex g_arena_mu;
+std::map<int, Arena> g_arenas;
+
+void* arena(int device, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_arena_mu);
+  Arena& a = g_arenas[device];
+  if (a.bytes < bytes) {
+    if (a.ptr) cudaFree(a.ptr);
+    a.ptr = nullptr;
+    a.bytes = 0;
+    check(cudaMalloc(&a.ptr, bytes), "cudaMalloc(workspace)");
+    a.bytes = bytes;
+  }
+  return a.ptr;
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+// carve consecutive aligned regions out of one allocation
+struct Carver {
+  char* base;
+  size_t off = 0;
+  template <class T>
+  T* take(size_t count) {
+    T* p = reinterpret_cast<T*>(base + off);
+    off += align_up(count * sizeof(T));
+    return p;
+  }
+};
+
+dev::PlanArgs plan_args(const Plan& plan, const DevicePlan* dp);
+
+}  // namespace
+
+struct DevicePlan {
+  int device = 0;
+  int32_t* term_info = nullptr;
+  uint32_t* pos = nullptr;
+  uint32_t* base = nullptr;
+  double* coeff = nullptr;
+};
+
+namespace {
+dev::PlanArgs plan_args(const Plan& plan, const DevicePlan* dp) {
+  dev::PlanArgs pa{};
+  pa.term_info = dp->term_info;
+  pa.pos = dp->pos;
+  pa.base = dp->base;
+  pa.coeff = dp->coeff;
+  pa.n = static_cast<int>(plan.dim);
+  pa.n_polys = static_cast<int>(plan.n_polys);
+  pa.n_terms = static_cast<int>(plan.n_terms());
+  return pa;
+}
+}  // namespace
+
+bool device_supports(uint32_t n, uint32_t max_k) { return pick_variant(1, n, max_k) != nullptr; }
+
+DevicePlan* device_plan_upload(const Plan& plan, int device) {
+  DeviceGuard g(device);
+  auto* dp = new DevicePlan;
+  dp->device = device;
+  try {
+    dp->term_info = upload(plan.term_info);
+    dp->pos = upload(plan.pos);
+    dp->base = upload(plan.base);
+    dp->coeff = upload(plan.coeff);
+  } catch (...) {
+    device_plan_free(dp);
+    throw;
+  }
+  return dp;
+}
+
+void device_plan_free(DevicePlan* dp) {
+  if (dp == nullptr) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(dp->device);
+  cudaFree(dp->term_info);
+  cudaFree(dp->pos);
+  cudaFree(dp->base);
+  cudaFree(dp->coeff);
+  if (prev >= 0) cudaSetDevice(prev);
+  delete dp;
+}
+
+// launch geometry of one tracking run: S slots in blocks of kBlock threads
+constexpr int kBlock = 128;
+
+size_t env_size(const char* name, size_t dflt) {
+  const char* v = std::getenv(name);
+  if (v == nullptr || *v == '\0') return dflt;
+  return static_cast<size_t>(std::strtoull(v, nullptr, 10));
+}
+
+void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_track_config& cfg,
+                  uint64_t lo, uint64_t hi, int device, pp_records* out, pp_run_stats* stats) {
+  auto wall0 = std::chrono::steady_clock::now();
+  DeviceGuard g(device);
+  const uint32_t n = plan.dim;
+  const uint32_t L = plan.L;
+  const dev::Variant* var = pick_variant(plan.prec, n, plan.max_k);
+  if (var == nullptr) throw InvalidArgument("system dimension / monomial size beyond the compiled kernels (n <= 32)");
+  const uint64_t count = hi - lo;
+
+  cudaDeviceProp prop;
+  check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  const size_t eval_smem = static_cast<size_t>(kBlock) * 2 * n * 2 * L * sizeof(double);
+  check(cudaFuncSetAttribute(var->eval_trip, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(eval_smem)),
+        "cudaFuncSetAttribute");
+  // slots: PP200_SLOTS_PER_SM (default 512) per SM, never more than the paths (whole blocks)
+  const size_t per_sm = std::max<size_t>(kBlock, env_size("PP200_SLOTS_PER_SM", 512));
+  uint64_t blocks = (per_sm / kBlock) * static_cast<uint64_t>(prop.multiProcessorCount);
+  blocks = std::min<uint64_t>(blocks, (count + kBlock - 1) / kBlock);
+  blocks = std::max<uint64_t>(blocks, 1);
+  const size_t S = blocks * kBlock;
+
+  const size_t cw = 2 * L;  // doubles per complex
+  const size_t nJ = static_cast<size_t>(n) * n, nR = static_cast<size_t>(n) * (n + 1) / 2;
+  const size_t kH = dev::kHistDepth;
+  const size_t graph_trips = std::max<size_t>(1, env_size("PP200_GRAPH_TRIPS", 16));
+  size_t bytes = 0;
+  auto room = [&](size_t b) { bytes += align_up(b); };
+  room(dev::kIntFields * S * 4);
+  room(S * 8);
+  room(dev::kRealFields * L * S * 8);
+  room(dev::kDblFields * S * 8);
+  for (size_t elems : {static_cast<size_t>(n), nJ, nR, static_cast<size_t>(n), static_cast<size_t>(n),
+                       static_cast<size_t>(n), kH * n})
+    room(elems * cw * S * 8);
+  room(kH * L * S * 8);
+  const size_t rec_bytes_x = count * n * cw * sizeof(double);
+  room(rec_bytes_x);
+  room(count * L * 8);
+  room(count);
+  room(count);
+  room(count * 4);
+  room(count * 4);
+  room(count * 4);
+  room(count * 4 * 8);
+  room(count);
+  room(64);
+  room(graph_trips * 4);
+  Carver cv{static_cast<char*>(arena(device, bytes))};
+
+  dev::TrackArgs a{};
+  a.plan = plan_args(plan, dp);
+  a.total_degree = st.total_degree ? 1 : 0;
+  a.rtol = cfg.residual_tol;
+  a.utol = cfg.update_tol;
+  a.h_init = cfg.h_init;
+  a.h_min = cfg.h_min;
+  a.h_max = cfg.h_max;
+  a.expand = cfg.expand;
+  a.contract = cfg.contract;
+  a.div_bound = cfg.divergence_bound;
+  a.rank_tol = default_rank_tol(plan.prec);
+  a.max_newton = cfg.max_newton;
+  a.expand_after = cfg.expand_after;
+  a.max_steps = cfg.max_steps;
+  a.lo = lo;
+  a.hi = hi;
+  a.S = S;
+  a.si = cv.take<int32_t>(dev::kIntFields * S);
+  a.spath = cv.take<unsigned long long>(S);
+  a.sr = cv.take<double>(dev::kRealFields * L * S);
+  a.sd = cv.take<double>(dev::kDblFields * S);
+  a.x = cv.take<double>(n * cw * S);
+  a.J = cv.take<double>(nJ * cw * S);
+  a.Rm = cv.take<double>(nR * cw * S);
+  a.B = cv.take<double>(n * cw * S);
+  a.Y = cv.take<double>(n * cw * S);
+  a.xacc = cv.take<double>(n * cw * S);
+  a.hx = cv.take<double>(kH * n * cw * S);
+  a.ht = cv.take<double>(kH * L * S);
+  a.rec_x = cv.take<double>(count * n * cw);
+  a.rec_res = cv.take<double>(count * L);
+  a.rec_status = cv.take<int8_t>(count);
+  a.rec_reason = cv.take<uint8_t>(count);
+  a.rec_steps = cv.take<uint32_t>(count);
+  a.rec_newton = cv.take<uint32_t>(count);
+  a.rec_rej = cv.take<uint32_t>(count);
+  a.rec_div = cv.take<double>(count * 4);
+  a.rec_divflag = cv.take<uint8_t>(count);
+  a.next = cv.take<unsigned long long>(8);
+  unsigned* busy = cv.take<unsigned>(graph_trips);
+
+  cudaStream_t stream;
+  check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
+  cudaEvent_t e0, e1, e2, e3;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventCreate(&e2);
+  cudaEventCreate(&e3);
+
+  // start tables (small): uploaded per call; explicit start lists only for [lo, hi)
+  std::vector<void*> temps;
+  uint64_t h2d = 0;
+  auto up = [&](const void* src, size_t b) -> void* {
+    void* p = nullptr;
+    check(cudaMallocAsync(&p, b == 0 ? 1 : b, stream), "cudaMallocAsync");
+    if (b) check(cudaMemcpyAsync(p, src, b, cudaMemcpyHostToDevice, stream), "H2D");
+    temps.push_back(p);
+    h2d += b;
+    return p;
+  };
+  cudaEventRecord(e0, stream);
+  if (st.total_degree) {
+    a.degrees = static_cast<const uint32_t*>(up(st.degrees.data(), st.degrees.size() * 4));
+    a.root_off = static_cast<const uint32_t*>(up(st.root_off.data(), st.root_off.size() * 4));
+    a.roots = static_cast<const double*>(up(st.roots.data(), st.roots.size() * 8));
+  } else {
+    a.explicit_x = static_cast<const double*>(up(st.explicit_x.data() + lo * n * cw, count * n * cw * 8));
+  }
+  cudaEventRecord(e1, stream);
+  check(cudaMemsetAsync(a.si, 0, dev::kIntFields * S * 4, stream), "memset");  // all slots M_IDLE
+  check(cudaMemsetAsync(a.next, 0, 8 * sizeof(unsigned long long), stream), "memset");
+
+  const dim3 grid(static_cast<unsigned>(blocks)), blk(kBlock);
+  void* targs[] = {&a};
+  unsigned* busy_slot = busy;
+  void* sargs[] = {&a, &busy_slot};
+  // seeding pass: every slot takes its first path
+  check(cudaLaunchKernel(var->step_trip, grid, blk, sargs, 0, stream), "launch step_trip");
+
+  // one trip = evaluate, solve, control; trips are captured G at a time into a CUDA graph whose
+  // last control kernel reports how many slots are still busy
+  cudaGraph_t graph;
+  check(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "capture");
+  check(cudaMemsetAsync(busy, 0, graph_trips * sizeof(unsigned), stream), "memset busy");
+  std::vector<unsigned*> busy_ptrs(graph_trips);
+  std::vector<void*> step_args(2 * graph_trips);
+  for (size_t j = 0; j < graph_trips; ++j) {
+    busy_ptrs[j] = busy + j;
+    void* sa[] = {&a, &busy_ptrs[j]};
+    check(cudaLaunchKernel(var->eval_trip, grid, blk, targs, eval_smem, stream), "launch eval_trip");
+    check(cudaLaunchKernel(var->lsq_trip, grid, blk, targs, 0, stream), "launch lsq_trip");
+    check(cudaLaunchKernel(var->step_trip, grid, blk, sa, 0, stream), "launch step_trip");
+  }
+  check(cudaStreamEndCapture(stream, &graph), "end capture");
+  cudaGraphExec_t exec;
+  check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
+  unsigned* h_busy = nullptr;
+  check(cudaMallocHost(&h_busy, sizeof(unsigned)), "cudaMallocHost");
+  uint64_t trips = 0, launches = 1;
+  for (;;) {
+    check(cudaGraphLaunch(exec, stream), "graph launch");
+    check(cudaMemcpyAsync(h_busy, busy + graph_trips - 1, sizeof(unsigned), cudaMemcpyDeviceToHost, stream), "D2H");
+    check(cudaStreamSynchronize(stream), "tracker trips");
+    trips += graph_trips;
+    launches += 3 * graph_trips;
+    if (*h_busy == 0) break;
+  }
+  cudaEventRecord(e2, stream);
+
+  // records back to the caller's host buffers
+  std::vector<double> div(count * 4);
+  std::vector<uint8_t> divflag(count);
+  auto down = [&](void* dst, const void* src, size_t b) {
+    if (b) check(cudaMemcpyAsync(dst, src, b, cudaMemcpyDeviceToHost, stream), "D2H");
+  };
+  down(out->x, a.rec_x, rec_bytes_x);
+  down(out->residual, a.rec_res, count * L * sizeof(double));
+  down(out->status, a.rec_status, count);
+  down(out->reason, a.rec_reason, count);
+  down(out->steps, a.rec_steps, count * 4);
+  down(out->newton_iters, a.rec_newton, count * 4);
+  down(out->rejections, a.rec_rej, count * 4);
+  down(div.data(), a.rec_div, count * 4 * sizeof(double));
+  down(divflag.data(), a.rec_divflag, count);
+  cudaEventRecord(e3, stream);
+  for (void* p : temps) cudaFreeAsync(p, stream);
+  check(cudaStreamSynchronize(stream), "record download");
+  float ms_h2d = 0, ms_k = 0, ms_d2h = 0;
+  cudaEventElapsedTime(&ms_h2d, e0, e1);
+  cudaEventElapsedTime(&ms_k, e1, e2);
+  cudaEventElapsedTime(&ms_d2h, e2, e3);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  cudaEventDestroy(e3);
+  cudaGraphExecDestroy(exec);
+  cudaGraphDestroy(graph);
+  cudaFreeHost(h_busy);
+  cudaStreamDestroy(stream);
+
+  // terminal divergence classification: m_est = log(growth) / log(shrink) with the host libm
+  // (tracker.cpp:429-431)
+  uint64_t newton_sum = 0;
+  for (uint64_t i = 0; i < count; ++i) {
+    out->path_id[i] = lo + i;
+    newton_sum += out->newton_iters[i];
+    if (!divflag[i]) continue;
+    const double first = div[i * 4 + 0], last = div[i * 4 + 1], uf = div[i * 4 + 2], ul = div[i * 4 + 3];
+    const double m_est = std::log(last / first) / std::log(uf / ul);
+    if (last >= 10.0 && m_est >= 0.05) out->reason[i] = PP_REASON_DIVERGED;
+  }
+  out->count = count;
+  if (stats) {
+    stats->paths = count;
+    stats->batches = 1;
+    stats->total_rounds = trips;
+    stats->newton_iters = newton_sum;
+    stats->device_ms = ms_k;
+    stats->h2d_ms = ms_h2d;
+    stats->d2h_ms = ms_d2h;
+    stats->h2d_bytes = h2d;
+    stats->d2h_bytes = rec_bytes_x + count * (L * 8 + 2 + 12 + 33);
+    stats->slots = static_cast<uint32_t>(S);
+    stats->kernel_launches = static_cast<uint32_t>(launches);
+    stats->wall_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// kernel-level parity entry points (host <-> planar transposition happens here)
+// ---------------------------------------------------------------------------------------------
+namespace {
+// user layout [item][elem][2L]  <->  planar [elem][plane][item]
+void to_planar(const double* src, double* dst, size_t items, size_t elems, size_t w) {
+  for (size_t i = 0; i < items; ++i)
+    for (size_t e = 0; e < elems; ++e)
+      for (size_t p = 0; p < w; ++p) dst[(e * w + p) * items + i] = src[(i * elems + e) * w + p];
+}
+void from_planar(const double* src, double* dst, size_t items, size_t elems, size_t w) {
+  for (size_t i = 0; i < items; ++i)
+    for (size_t e = 0; e < elems; ++e)
+      for (size_t p = 0; p < w; ++p) dst[(i * elems + e) * w + p] = src[(e * w + p) * items + i];
+}
+}  // namespace
+
+void device_eval(const Plan& plan, DevicePlan* dp, uint32_t batch, const double* points,
+                 const double* t, double* sys, double* jac, int device) {
+  if (batch == 0) return;
+  DeviceGuard g(device);
+  const uint32_t n = plan.dim, np = plan.n_polys, L = plan.L, w = 2 * L;
+  const dev::Variant* var = pick_variant(plan.prec, n, plan.max_k);
+  if (var == nullptr) throw InvalidArgument("system beyond the compiled kernels");
+  std::vector<double> xp(static_cast<size_t>(batch) * n * w), tp(static_cast<size_t>(batch) * L);
+  to_planar(points, xp.data(), batch, n, w);
+  to_planar(t, tp.data(), batch, 1, L);
+  double* dx = upload(xp);
+  double* dt = upload(tp);
+  double* ds = dmalloc<double>(static_cast<size_t>(batch) * np * w);
+  double* dj = dmalloc<double>(static_cast<size_t>(batch) * np * n * w);
+  dev::EvalArgs a{};
+  a.plan = plan_args(plan, dp);
+  a.batch = batch;
+  a.x = dx;
+  a.t = dt;
+  a.sys = ds;
+  a.jac = dj;
+  const int block = 128;
+  const size_t smem = static_cast<size_t>(block) * 2 * n * w * sizeof(double);
+  check(cudaFuncSetAttribute(var->eval, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)), "attr");
+  void* args[] = {&a};
+  check(cudaLaunchKernel(var->eval, dim3((batch + block - 1) / block), dim3(block), args, smem, 0), "launch eval");
+  check(cudaDeviceSynchronize(), "eval kernel");
+  std::vector<double> hs(static_cast<size_t>(batch) * np * w), hj(static_cast<size_t>(batch) * np * n * w);
+  check(cudaMemcpy(hs.data(), ds, hs.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+  check(cudaMemcpy(hj.data(), dj, hj.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+  cudaFree(dx);
+  cudaFree(dt);
+  cudaFree(ds);
+  cudaFree(dj);
+  from_planar(hs.data(), sys, batch, np, w);
+  if (jac) {
+    // planar element v*np + p  ->  user row p*n + v
+    for (size_t i = 0; i < batch; ++i)
+      for (size_t p = 0; p < np; ++p)
+        for (size_t v = 0; v < n; ++v)
+          for (size_t q = 0; q < w; ++q)
+            jac[((i * np + p) * n + v) * w + q] = hj[((v * np + p) * w + q) * batch + i];
+  }
+}
+
+void device_lsq(int prec, uint32_t n, uint32_t batch, const double* a, const double* b, double* x,
+                uint8_t* ok, int device) {
+  if (batch == 0) return;
+  DeviceGuard g(device);
+  const uint32_t L = prec == 0 ? 1 : (prec == 1 ? 2 : 4), w = 2 * L;
+  const dev::Variant* var = pick_variant(prec, n, 2);
+  if (var == nullptr) throw InvalidArgument("least-squares size beyond the compiled kernels");
+  std::vector<double> ap(static_cast<size_t>(batch) * n * n * w), bp(static_cast<size_t>(batch) * n * w);
+  to_planar(a, ap.data(), batch, static_cast<size_t>(n) * n, w);
+  to_planar(b, bp.data(), batch, n, w);
+  double* da = upload(ap);
+  double* db = upload(bp);
+  double* dr = dmalloc<double>(static_cast<size_t>(batch) * n * (n + 1) / 2 * w);
+  double* dy = dmalloc<double>(static_cast<size_t>(batch) * n * w);
+  double* dxv = dmalloc<double>(static_cast<size_t>(batch) * n * w);
+  uint8_t* dok = dmalloc<uint8_t>(batch);
+  dev::LsqArgs args{static_cast<int>(n), batch, default_rank_tol(prec), da, dr, db, dy, dxv, dok};
+  void* pa[] = {&args};
+  const int block = 128;
+  check(cudaLaunchKernel(var->lsq, dim3((batch + block - 1) / block), dim3(block), pa, 0, 0), "launch lsq");
+  check(cudaDeviceSynchronize(), "lsq kernel");
+  std::vector<double> hx(static_cast<size_t>(batch) * n * w);
+  check(cudaMemcpy(hx.data(), dxv, hx.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+  check(cudaMemcpy(ok, dok, batch, cudaMemcpyDeviceToHost), "D2H");
+  for (void* p : {static_cast<void*>(da), static_cast<void*>(db), static_cast<void*>(dr),
+                  static_cast<void*>(dy), static_cast<void*>(dxv), static_cast<void*>(dok)})
+    cudaFree(p);
+  from_planar(hx.data(), x, batch, n, w);
+}
+
+}  // namespace pp

@@ -1,0 +1,39 @@
+// device.hpp -- internal interface between the host C ABI (capi.cpp) and the CUDA side.
+#pragma once
+
+#include <string>
+
+#include "host.hpp"
+#include "pp200.h"
+
+namespace pp {
+
+// Thrown by the CUDA side on any runtime failure; mapped to PP_E_CUDA at the C ABI.
+struct CudaFailure : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// Device-resident copy of a plan (SoA tables), built once per homotopy and reused by every call.
+struct DevicePlan;
+DevicePlan* device_plan_upload(const Plan& plan, int device);
+void device_plan_free(DevicePlan* dp);
+
+// track_all on the device: starts [lo, hi) -> records (host buffers in `out`).
+void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_track_config& cfg,
+                  uint64_t lo, uint64_t hi, int device, pp_records* out, pp_run_stats* stats);
+
+// eval_system_batch on the device (host buffers, layouts of pp_eval_batch)
+void device_eval(const Plan& plan, DevicePlan* dp, uint32_t batch, const double* points,
+                 const double* t, double* sys, double* jac, int device);
+
+// batched least_squares_solve (layouts of pp_lsq_batch)
+void device_lsq(int prec, uint32_t n, uint32_t batch, const double* a, const double* b, double* x,
+                uint8_t* ok, int device);
+
+// rank tolerance of the reference's least_squares_solve default (linalg.hpp:44-52)
+inline double default_rank_tol(int prec) { return prec == 0 ? 1e-8 : (prec == 1 ? 1e-16 : 1e-32); }
+
+// largest dimension / monomial support the compiled kernels cover
+bool device_supports(uint32_t n, uint32_t max_k);
+
+}  // namespace pp

@@ -1,0 +1,101 @@
+// kernels.hpp -- argument blocks and the registry of compiled kernel variants.
+//
+// Kernels are templated on the level R (double / dd / qd), NMAX (largest system dimension the
+// register-resident Gram-Schmidt column covers) and KMAX (largest number of distinct variables in
+// a monomial, i.e. the length of the Speelpenning prefix stack kept in registers).  Each
+// precision's variants live in their own translation unit (track_d.cu, track_dd.cu, track_qd.cu)
+// so they compile in parallel.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+namespace pp {
+namespace dev {
+
+constexpr int kHistDepth = 5;  // predictor history depth (reference tracker.cpp:87)
+// slot-state field counts (enums F_*, R_*, D_* in track_impl.cuh)
+constexpr int kIntFields = 14, kRealFields = 4, kDblFields = 3;
+
+// Plan tables, device pointers (layouts documented in host.hpp, struct Plan)
+struct PlanArgs {
+  const int32_t* term_info;  // 4 per term
+  const uint32_t* pos;
+  const uint32_t* base;
+  const double* coeff;       // per term: c_start (2L) then c_target (2L)
+  int n;                     // variables
+  int n_polys;
+  int n_terms;
+};
+
+// One persistent launch of the path tracker.
+struct TrackArgs {
+  PlanArgs plan;
+  // start data: total degree (roots) or explicit list
+  int total_degree;
+  const uint32_t* degrees;
+  const uint32_t* root_off;
+  const double* roots;
+  const double* explicit_x;
+  // TrackConfig (tracker.hpp:29-46) + rank tolerance (linalg.hpp:44-52)
+  double rtol, utol, h_init, h_min, h_max, expand, contract, div_bound, rank_tol;
+  int max_newton, expand_after;
+  uint32_t max_steps;
+  // start-index range and refill counter
+  unsigned long long lo, hi;
+  unsigned long long* next;
+  // per-slot storage (S slots).  Planar arrays: element e, limb-plane p, slot s at ((e*P)+p)*S+s.
+  size_t S;
+  int32_t* si;                  // integer state, field f at f*S + s (track_impl.cuh F_*)
+  unsigned long long* spath;    // start index owned by the slot
+  double* sr;                   // level-R scalars (t, h, t_next, final residual), planar real
+  double* sd;                   // double scalars (residual, |dx|, |x|) at f*S + s
+  double *x, *J, *Rm, *B, *Y, *xacc, *hx, *ht;
+  // records, indexed by start index - lo
+  double* rec_x;       // [rec][n][2L]
+  double* rec_res;     // [rec][L]
+  int8_t* rec_status;
+  uint8_t* rec_reason;
+  uint32_t *rec_steps, *rec_newton, *rec_rej;
+  double* rec_div;     // [rec][4]: first, last, u_first, u_last of the terminal-divergence test
+  uint8_t* rec_divflag;
+};
+
+// eval_system_batch for independent points (one thread per point)
+struct EvalArgs {
+  PlanArgs plan;
+  uint32_t batch;
+  const double* x;  // planar, S = batch: element v (n of them)
+  const double* t;  // planar real, element 0
+  double* sys;      // planar, element p (n_polys)
+  double* jac;      // planar, element v*n_polys + p (column-major Jacobian)
+};
+
+// least_squares_solve for independent systems (one thread per system)
+struct LsqArgs {
+  int n;
+  uint32_t batch;
+  double rank_tol;
+  double* a;   // planar, element col*n + row (overwritten by Q)
+  double* r;   // planar, packed upper triangle, n(n+1)/2
+  double* b;   // planar, element row
+  double* y;   // planar scratch, n
+  double* x;   // planar out, n
+  uint8_t* ok;
+};
+
+struct Variant {
+  int nmax, kmax;
+  const void* eval_trip;  // __global__ void(TrackArgs)
+  const void* lsq_trip;   // __global__ void(TrackArgs)
+  const void* step_trip;  // __global__ void(TrackArgs, unsigned* busy)
+  const void* eval;       // __global__ void(EvalArgs)
+  const void* lsq;        // __global__ void(LsqArgs)
+};
+
+const Variant* variants_d(int* count);
+const Variant* variants_dd(int* count);
+const Variant* variants_qd(int* count);
+
+}  // namespace dev
+}  // namespace pp

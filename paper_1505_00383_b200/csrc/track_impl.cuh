@@ -1,0 +1,687 @@
+// track_impl.cuh -- sm_100a kernels of the many-path tracker.
+//
+// Design: one CUDA thread owns one path slot for the whole launch (persistent
+// grid, one wave).  A slot runs the reference's per-path state machine -- predict, up to
+// max_newton corrector iterations, step control, status, finalize -- and refills itself from a
+// global atomic start counter when its path ends, so paths that finish or diverge release their
+// thread immediately (the reference's compaction, tracker.cpp:340-387, without a host round trip).
+// Every loop trip performs exactly one "heavy" operation per slot -- an evaluation of H and
+// dH/dx at the slot's point followed (in corrector/refinement modes) by a least-squares solve --
+// so all lanes of a warp execute the expensive code together even though each lane is at a
+// different place on a different path; only the cheap bookkeeping between trips diverges.
+//
+// Per-path results are bitwise identical to the reference CPU tracker: every floating-point
+// operation is the reference's (xprec.cuh), executed in the reference's order per path, and the
+// reference's per-path results do not depend on batching (test_tracker.cpp:383-432).
+//
+// Memory: the working point x and the open Jacobian row live in shared memory (dynamic indices
+// from the instruction tables); the Jacobian / Q, R, right-hand side, history and accepted point
+// live in global memory in a slot-minor planar layout (element e, limb-plane p, slot s at
+// ((e*P)+p)*S+s) so a warp's 32 slots touch 32 consecutive doubles -- the paper's transposed
+// layout (Table 5/7).  The Gram-Schmidt column being orthogonalised and the Speelpenning
+// prefix products are register arrays (NMAX / KMAX).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "kernels.hpp"
+#include "xprec.cuh"
+
+namespace pp {
+namespace dev {
+
+enum : int { M_IDLE = 0, M_NEWTON = 1, M_REFINE = 2, M_FINAL = 3, M_DONE = 4 };
+enum : int { ST_FAILED = -1, ST_ACTIVE = 0, ST_SUCCESS = 1 };
+enum : int { RS_NONE = 0, RS_DIVERGED = 1, RS_UNDERFLOW = 2, RS_MAXSTEPS = 3, RS_SINGULAR = 4, RS_NOCERT = 5 };
+constexpr int kHist = kHistDepth;
+
+// ---------------------------------------------------------------------------------------------
+// planar accessors
+// ---------------------------------------------------------------------------------------------
+template <class R>
+struct Planar {
+  static constexpr int L = level<R>::L;
+  double* base;
+  size_t S;  // stride between planes (slots, or blockDim for shared memory)
+
+  __device__ __forceinline__ cx<R> ld(int e, size_t s) const {
+    cx<R> z;
+    const double* p = base + (static_cast<size_t>(e) * 2 * L) * S + s;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      level<R>::set(z.re, l, p[l * S]);
+      level<R>::set(z.im, l, p[(L + l) * S]);
+    }
+    return z;
+  }
+  __device__ __forceinline__ void st(int e, size_t s, const cx<R>& z) const {
+    double* p = base + (static_cast<size_t>(e) * 2 * L) * S + s;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      p[l * S] = level<R>::get(z.re, l);
+      p[(L + l) * S] = level<R>::get(z.im, l);
+    }
+  }
+  // real-valued elements (L planes each)
+  __device__ __forceinline__ R ldr(int e, size_t s) const {
+    R v;
+    const double* p = base + (static_cast<size_t>(e) * L) * S + s;
+#pragma unroll
+    for (int l = 0; l < L; ++l) level<R>::set(v, l, p[l * S]);
+    return v;
+  }
+  __device__ __forceinline__ void str(int e, size_t s, const R& v) const {
+    double* p = base + (static_cast<size_t>(e) * L) * S + s;
+#pragma unroll
+    for (int l = 0; l < L; ++l) p[l * S] = level<R>::get(v, l);
+  }
+};
+
+// uniform (warp-broadcast) load of a complex table entry stored as 2L consecutive doubles
+template <class R>
+__device__ __forceinline__ cx<R> ld_table(const double* p) {
+  constexpr int L = level<R>::L;
+  cx<R> z;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    level<R>::set(z.re, l, __ldg(p + l));
+    level<R>::set(z.im, l, __ldg(p + L + l));
+  }
+  return z;
+}
+
+template <class R>
+__device__ __forceinline__ void st_flat(double* p, const cx<R>& z) {
+  constexpr int L = level<R>::L;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    p[l] = level<R>::get(z.re, l);
+    p[L + l] = level<R>::get(z.im, l);
+  }
+}
+
+template <class R>
+__device__ __forceinline__ cx<R> ld_flat(const double* p) {
+  constexpr int L = level<R>::L;
+  cx<R> z;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    level<R>::set(z.re, l, __ldg(p + l));
+    level<R>::set(z.im, l, __ldg(p + L + l));
+  }
+  return z;
+}
+
+// ---------------------------------------------------------------------------------------------
+// evaluation of H(x, t) and dH/dx (reference evaldiff.cpp:259-374, fused per term)
+// ---------------------------------------------------------------------------------------------
+// X: the point (shared memory, this thread's column); JR: open Jacobian row accumulator (shared);
+// outputs: B[p] = -H_p (the least-squares right-hand side, tracker.cpp:249), J[v*n_polys + p];
+// resid_d = max_p to_double(|H_p|) (tracker.cpp:247-251), resid_r = max_p |H_p| at level R
+// (tracker.cpp:488-494).  The coefficient, monomial and sum stages of the reference are fused: the
+// value/derivative slots of one term are produced in registers and accumulated immediately.
+// Because the plan is polynomial-major (evaldiff.cpp:200-236), only one row of H/J is open.
+template <class R, int KMAX>
+__device__ void eval_hj(const PlanArgs& pa, const Planar<R>& X, const Planar<R>& JR, size_t ls,
+                        const R& t, const Planar<R>& B, const Planar<R>& J, size_t gs,
+                        double& resid_d, R& resid_r) {
+  constexpr int L = level<R>::L;
+  const int n = pa.n, np = pa.n_polys;
+  const cx<R> zero = czero<R>();
+  const R u = rsub(rfrom<R>(1.0), t);  // ws.set_t: 1 - t at level R (evaldiff.hpp:198-201)
+
+  for (int v = 0; v < n; ++v) JR.st(v, ls, zero);
+  cx<R> sacc = zero;
+  resid_d = 0.0;
+  resid_r = rfrom<R>(0.0);
+  int cur = 0;
+
+  auto flush = [&](int p) {
+    B.st(p, gs, cneg(sacc));
+    R m = cabsr(sacc);
+    resid_d = f_max(resid_d, rtod(m));
+    if (rcmp(m, resid_r) > 0) resid_r = m;
+    for (int v = 0; v < n; ++v) {
+      J.st(v * np + p, gs, JR.ld(v, ls));
+      JR.st(v, ls, zero);
+    }
+    sacc = zero;
+  };
+
+  for (int i = 0; i < pa.n_terms; ++i) {
+    const int4 ti = __ldg(reinterpret_cast<const int4*>(pa.term_info) + i);
+    const int poly = ti.x, k = ti.y, po = ti.z, nb = ti.w & 0xff, bo = ti.w >> 8;
+    while (cur < poly) flush(cur++);
+
+    // coefficient stage: c = c_start*(1-t) + c_target*t (evaldiff.cpp:259-274)
+    const double* cp = pa.coeff + static_cast<size_t>(i) * 4 * L;
+    const cx<R> cs = ld_table<R>(cp), ct = ld_table<R>(cp + 2 * L);
+    const cx<R> c{radd(rmul(cs.re, u), rmul(ct.re, t)), radd(rmul(cs.im, u), rmul(ct.im, t))};
+
+    if (k == 0) {  // constants skip the monomial stage (evaldiff.cpp:345-352)
+      sacc = cadd(sacc, c);
+      continue;
+    }
+
+    // common factor prod x^(e-1) by square-and-multiply (evaldiff.cpp:119-161)
+    cx<R> aux = zero;
+    if (nb > 0) {
+      bool init = false;
+      for (int b = 0; b < nb; ++b) {
+        const uint32_t be = __ldg(pa.base + bo + b);
+        const cx<R> xv = X.ld(static_cast<int>(be & 0xffffu), ls);
+        const uint32_t e = be >> 16;
+        if (e == 1) {
+          aux = init ? cmul(aux, xv) : xv;
+          init = true;
+          continue;
+        }
+        cx<R> sq = xv;
+        for (uint32_t bits = e; bits != 0;) {
+          if (bits & 1u) {
+            aux = init ? cmul(aux, sq) : sq;
+            init = true;
+          }
+          bits >>= 1;
+          if (bits != 0) sq = cmul(sq, sq);
+        }
+      }
+    }
+
+    const uint32_t* pv = pa.pos + po;
+    // derivative contribution w = c*d (scaled by the exponent when e != 1) into row entry var
+    auto contribute = [&](uint32_t pe, cx<R> d) {
+      if (nb > 0) d = cmul(d, aux);
+      cx<R> w = cmul(c, d);
+      const uint32_t e = pe >> 16;
+      if (e != 1) w = cmuld(w, static_cast<double>(e));
+      const int var = static_cast<int>(pe & 0xffffu);
+      JR.st(var, ls, cadd(JR.ld(var, ls), w));
+    };
+
+    if (k == 1) {
+      const uint32_t p0 = __ldg(pv);
+      cx<R> val = X.ld(static_cast<int>(p0 & 0xffffu), ls);
+      if (nb > 0) val = cmul(val, aux);
+      sacc = cadd(sacc, cmul(c, val));
+      contribute(p0, cone<R>());
+      continue;
+    }
+
+    // Speelpenning products (evaldiff.cpp:90-115): prefix P_j = x_p0 ... x_p(j-1) for j < k,
+    // value = P_(k-1) x_p(k-1), d_j = P_j * S_(j+1) with the running suffix S.
+    cx<R> P[KMAX > 1 ? KMAX : 2];
+    cx<R> run = X.ld(static_cast<int>(__ldg(pv) & 0xffffu), ls);
+    P[1] = run;
+#pragma unroll
+    for (int j = 2; j < KMAX; ++j) {
+      if (j < k) {
+        run = cmul(run, X.ld(static_cast<int>(__ldg(pv + j - 1) & 0xffffu), ls));
+        P[j] = run;
+      }
+    }
+    const uint32_t plast = __ldg(pv + k - 1);
+    const cx<R> xlast = X.ld(static_cast<int>(plast & 0xffffu), ls);
+    cx<R> val = cmul(run, xlast);
+    if (nb > 0) val = cmul(val, aux);
+    sacc = cadd(sacc, cmul(c, val));
+    contribute(plast, run);  // d_(k-1) = P_(k-1)
+    cx<R> acc = xlast;
+#pragma unroll
+    for (int j = KMAX - 2; j >= 1; --j) {
+      if (j <= k - 2) {
+        const uint32_t pj = __ldg(pv + j);
+        const cx<R> d = cmul(P[j], acc);
+        acc = cmul(acc, X.ld(static_cast<int>(pj & 0xffffu), ls));
+        contribute(pj, d);
+      }
+    }
+    contribute(__ldg(pv), acc);  // d_0 = S_1
+  }
+  while (cur < np) flush(cur++);
+}
+
+// ---------------------------------------------------------------------------------------------
+// least squares by two-pass modified Gram-Schmidt (reference linalg.hpp:79-125)
+// ---------------------------------------------------------------------------------------------
+// Q: n x n column-major (element col*n + row), overwritten by the orthonormal factor;
+// Rm: packed upper triangle (element i + k(k+1)/2); B: right-hand side; Y: scratch (Q^H b).
+// Returns false on rank deficiency (r_kk <= rank_tol * max column norm).  The column being
+// orthogonalised is held in registers (NMAX); q_i columns stream from memory.
+template <class R, int NMAX>
+__device__ bool lsq_solve(int n, double rank_tol, const Planar<R>& Q, const Planar<R>& Rm,
+                          const Planar<R>& B, const Planar<R>& Y, size_t s, cx<R> (&dx)[NMAX]) {
+  const cx<R> zero = czero<R>();
+  R max_norm = rfrom<R>(0.0);
+  for (int j = 0; j < n; ++j) {
+    R acc = rfrom<R>(0.0);
+    for (int r = 0; r < n; ++r) acc = radd(acc, cabs2(Q.ld(j * n + r, s)));
+    const R nj = rsqrt(acc);
+    if (rcmp(nj, max_norm) > 0) max_norm = nj;
+  }
+  const R tol = rmul(max_norm, rfrom<R>(rank_tol));
+
+  for (int k = 0; k < n; ++k) {
+    cx<R> ck[NMAX];
+#pragma unroll
+    for (int r = 0; r < NMAX; ++r)
+      if (r < n) ck[r] = Q.ld(k * n + r, s);
+    const int rk = k * (k + 1) / 2;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int i = 0; i < k; ++i) {
+        cx<R> rik = zero;
+#pragma unroll
+        for (int r = 0; r < NMAX; ++r)
+          if (r < n) rik = cadd(rik, cmul(cconj(Q.ld(i * n + r, s)), ck[r]));
+        const cx<R> prev = pass == 0 ? zero : Rm.ld(i + rk, s);
+        Rm.st(i + rk, s, cadd(prev, rik));
+#pragma unroll
+        for (int r = 0; r < NMAX; ++r)
+          if (r < n) ck[r] = csub(ck[r], cmul(rik, Q.ld(i * n + r, s)));
+      }
+    }
+    R acc = rfrom<R>(0.0);
+#pragma unroll
+    for (int r = 0; r < NMAX; ++r)
+      if (r < n) acc = radd(acc, cabs2(ck[r]));
+    const R rkk = rsqrt(acc);
+    if (rcmp(rkk, tol) <= 0) return false;
+    Rm.st(k + rk, s, cx<R>{rkk, rfrom<R>(0.0)});
+    const R rinv = rdiv(rfrom<R>(1.0), rkk);
+    cx<R> y = zero;
+#pragma unroll
+    for (int r = 0; r < NMAX; ++r) {
+      if (r < n) {
+        ck[r] = cmulr(ck[r], rinv);
+        Q.st(k * n + r, s, ck[r]);
+        y = cadd(y, cmul(cconj(ck[r]), B.ld(r, s)));  // y_k = <q_k, b> (linalg.hpp:117)
+      }
+    }
+    Y.st(k, s, y);
+  }
+  // back substitution R x = y (linalg.hpp:118-122)
+#pragma unroll
+  for (int j = NMAX - 1; j >= 0; --j) {
+    if (j < n) {
+      cx<R> acc = Y.ld(j, s);
+#pragma unroll
+      for (int i = j + 1; i < NMAX; ++i)
+        if (i < n) acc = csub(acc, cmul(Rm.ld(j + i * (i + 1) / 2, s), dx[i]));
+      dx[j] = cdiv(acc, Rm.ld(j + j * (j + 1) / 2, s));
+    }
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------------------------------------
+// slot state (global, SoA): integer fields, path index, level-R scalars, double scalars
+// ---------------------------------------------------------------------------------------------
+enum : int {
+  F_MODE = 0, F_IT, F_RIT, F_LEN, F_HEAD, F_CONSEC, F_CORR, F_SING, F_STATUS, F_REASON,
+  F_STEPS, F_NEWTON, F_REJ, F_OK, F_COUNT
+};
+enum : int { R_T = 0, R_H, R_TNEXT, R_RESID, R_COUNT };     // level-R scalars (planar real)
+enum : int { D_RESID = 0, D_DXN, D_XN, D_COUNT };          // double scalars
+static_assert(F_COUNT == kIntFields && R_COUNT == kRealFields && D_COUNT == kDblFields, "state layout");
+
+struct SlotInts {
+  int32_t* base;
+  size_t S;
+  __device__ __forceinline__ int32_t& operator()(int f, size_t s) const { return base[f * S + s]; }
+};
+
+// ---------------------------------------------------------------------------------------------
+// trip kernel 1: evaluate H and dH/dx at every busy slot's point
+// ---------------------------------------------------------------------------------------------
+template <class R, int KMAX>
+__global__ void __launch_bounds__(128) eval_trip(const TrackArgs a) {
+  constexpr int L = level<R>::L;
+  extern __shared__ double smem[];
+  const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= a.S) return;
+  const SlotInts si{a.si, a.S};
+  const int mode = si(F_MODE, s);
+  if (mode != M_NEWTON && mode != M_REFINE && mode != M_FINAL) return;
+  const int n = a.plan.n;
+  const size_t ls = threadIdx.x;
+  const Planar<R> XS{smem, blockDim.x};
+  const Planar<R> JR{smem + static_cast<size_t>(n) * 2 * L * blockDim.x, blockDim.x};
+  const Planar<R> X{a.x, a.S}, SR{a.sr, a.S}, J{a.J, a.S}, B{a.B, a.S};
+  for (int v = 0; v < n; ++v) XS.st(v, ls, X.ld(v, s));
+  const R t = mode == M_NEWTON ? SR.ldr(R_TNEXT, s) : rfrom<R>(1.0);
+  double resid;
+  R resid_r;
+  eval_hj<R, KMAX>(a.plan, XS, JR, ls, t, B, J, s, resid, resid_r);
+  a.sd[D_RESID * a.S + s] = resid;
+  SR.str(R_RESID, s, resid_r);
+}
+
+// ---------------------------------------------------------------------------------------------
+// trip kernel 2: least-squares Newton update for corrector / refinement slots
+// ---------------------------------------------------------------------------------------------
+template <class R, int NMAX>
+__global__ void __launch_bounds__(128) lsq_trip(const TrackArgs a) {
+  const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= a.S) return;
+  const SlotInts si{a.si, a.S};
+  const int mode = si(F_MODE, s);
+  if (mode != M_NEWTON && mode != M_REFINE) return;
+  const int n = a.plan.n;
+  const Planar<R> X{a.x, a.S}, J{a.J, a.S}, Rm{a.Rm, a.S}, B{a.B, a.S}, Y{a.Y, a.S};
+  cx<R> dx[NMAX];
+  const bool ok = lsq_solve<R, NMAX>(n, a.rank_tol, J, Rm, B, Y, s, dx);
+  si(F_OK, s) = ok ? 1 : 0;
+  if (!ok) return;
+  // x += dx; update and iterate norms (tracker.cpp:258-264)
+  double dxn = 0.0, xn = 0.0;
+#pragma unroll
+  for (int v = 0; v < NMAX; ++v) {
+    if (v < n) {
+      const cx<R> xv = cadd(X.ld(v, s), dx[v]);
+      X.st(v, s, xv);
+      dxn = f_max(dxn, cabsd(dx[v]));
+      xn = f_max(xn, cabsd(xv));
+    }
+  }
+  a.sd[D_DXN * a.S + s] = dxn;
+  a.sd[D_XN * a.S + s] = xn;
+}
+
+// ---------------------------------------------------------------------------------------------
+// trip kernel 3: per-path control -- corrector bookkeeping, step control, status, prediction,
+// finalize and record output, refill from the start counter
+// ---------------------------------------------------------------------------------------------
+template <class R>
+__global__ void __launch_bounds__(128) step_trip(const TrackArgs a, unsigned* busy_out) {
+  constexpr int L = level<R>::L;
+  const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool in_range = s < a.S;
+  int mode = M_DONE;
+  if (in_range) {
+    const SlotInts si{a.si, a.S};
+    mode = si(F_MODE, s);
+    if (mode != M_DONE) {
+      const int n = a.plan.n;
+      const Planar<R> X{a.x, a.S}, SR{a.sr, a.S}, XA{a.xacc, a.S}, HX{a.hx, a.S}, HT{a.ht, a.S};
+      const R one = rfrom<R>(1.0);
+      unsigned long long path = a.spath[s];
+      int it = si(F_IT, s), rit = si(F_RIT, s), len = si(F_LEN, s), head = si(F_HEAD, s);
+      int consec = si(F_CONSEC, s), corrected = si(F_CORR, s), sing = si(F_SING, s);
+      int status = si(F_STATUS, s), reason = si(F_REASON, s);
+      uint32_t steps = si(F_STEPS, s), newton = si(F_NEWTON, s), rej = si(F_REJ, s);
+      const bool ok = si(F_OK, s) != 0;
+      R t = SR.ldr(R_T, s), h = SR.ldr(R_H, s), tnext = SR.ldr(R_TNEXT, s);
+
+      // predictor (tracker.cpp:178-214): t_next = min(t + h, 1); Lagrange extrapolation through
+      // the accepted history (oldest first), a copy when only the start point is known
+      auto predict = [&]() {
+        R tn = radd(t, h);
+        if (rcmp(tn, one) >= 0) tn = one;
+        tnext = tn;
+        if (len == 1) {
+          for (int v = 0; v < n; ++v) X.st(v, s, HX.ld(head * n + v, s));
+          return;
+        }
+        R ts[kHist], w[kHist];
+#pragma unroll
+        for (int i = 0; i < kHist; ++i)
+          if (i < len) ts[i] = HT.ldr((head + i) % kHist, s);
+#pragma unroll
+        for (int i = 0; i < kHist; ++i) {
+          if (i < len) {
+            R wi = one;
+#pragma unroll
+            for (int j = 0; j < kHist; ++j)
+              if (j < len && j != i) wi = rmul(wi, rdiv(rsub(tn, ts[j]), rsub(ts[i], ts[j])));
+            w[i] = wi;
+          }
+        }
+        for (int v = 0; v < n; ++v) {
+          cx<R> acc = czero<R>();
+#pragma unroll
+          for (int i = 0; i < kHist; ++i)
+            if (i < len) acc = cadd(acc, cmulr(HX.ld(((head + i) % kHist) * n + v, s), w[i]));
+          X.st(v, s, acc);
+        }
+      };
+
+      if (mode == M_NEWTON) {
+        ++it;
+        ++newton;
+        const double resid = a.sd[D_RESID * a.S + s];
+        const double dxn = a.sd[D_DXN * a.S + s], xn = a.sd[D_XN * a.S + s];
+        bool done = false;
+        if (!ok) {
+          sing = 1;  // this step failed (tracker.cpp:253-257)
+          done = true;
+        } else if (resid <= a.rtol && dxn <= f_mul(a.utol, f_max(1.0, xn))) {
+          corrected = 1;
+          done = true;
+        } else if (it >= a.max_newton) {
+          done = true;
+        }
+        if (done) {
+          // step control (tracker.cpp:293-317); history push with FIFO drop at depth 5
+          // (tracker.cpp:276-291) kept as a ring buffer
+          double xacc_norm = 0.0;
+          if (corrected) {
+            ++steps;
+            if (consec < 255) ++consec;
+            t = tnext;
+            if (len == kHist) {
+              head = (head + 1) % kHist;
+              len = kHist - 1;
+            }
+            const int at = (head + len) % kHist;
+            HT.str(at, s, tnext);
+            for (int v = 0; v < n; ++v) {
+              const cx<R> xv = X.ld(v, s);
+              XA.st(v, s, xv);
+              HX.st(at * n + v, s, xv);
+            }
+            ++len;
+            if (consec >= a.expand_after) {
+              const R grown = rmuld(h, a.expand);
+              h = rcmp(grown, rfrom<R>(a.h_max)) > 0 ? rfrom<R>(a.h_max) : grown;
+            }
+            xacc_norm = xn;  // norm of the accepted point = the last iterate's norm
+          } else {
+            ++rej;
+            consec = 0;
+            h = rmuld(h, a.contract);
+            for (int v = 0; v < n; ++v) xacc_norm = f_max(xacc_norm, cabsd(XA.ld(v, s)));
+          }
+          // status on the accepted point (tracker.cpp:319-338)
+          if (xacc_norm > a.div_bound) {
+            status = ST_FAILED;
+            reason = RS_DIVERGED;
+          } else if (rcmp(h, rfrom<R>(a.h_min)) < 0) {
+            status = ST_FAILED;
+            reason = sing ? RS_SINGULAR : RS_UNDERFLOW;
+          } else if (steps > a.max_steps) {
+            status = ST_FAILED;
+            reason = RS_MAXSTEPS;
+          } else if (rcmp(t, one) == 0 && corrected) {
+            status = ST_SUCCESS;
+          }
+
+          if (status == ST_ACTIVE) {
+            predict();
+            it = 0;
+            corrected = 0;
+            sing = 0;
+          } else {
+            const size_t rec = static_cast<size_t>(path - a.lo);
+            uint8_t flag = 0;
+            if (status == ST_FAILED && reason != RS_DIVERGED && f_sub(1.0, rtod(t)) < 0.01 && len >= 3) {
+              // terminal divergence test inputs (tracker.cpp:406-432); the log ratio is taken on
+              // the host with the reference's libm
+              double first = 0.0, prev = -1.0, last = 0.0;
+              bool growing = true;
+              for (int i = 0; i < len; ++i) {
+                double nrm = 0.0;
+                const int at = (head + i) % kHist;
+                for (int v = 0; v < n; ++v) nrm = f_max(nrm, cabsd(HX.ld(at * n + v, s)));
+                if (nrm <= prev) growing = false;
+                if (i == 0) first = nrm;
+                prev = nrm;
+                last = nrm;
+              }
+              const double uf = f_sub(1.0, rtod(HT.ldr(head, s)));
+              const double ul = f_sub(1.0, rtod(HT.ldr((head + len - 1) % kHist, s)));
+              if (growing && first > 0.0 && ul > 0.0 && uf > ul) {
+                flag = 1;
+                a.rec_div[rec * 4 + 0] = first;
+                a.rec_div[rec * 4 + 1] = last;
+                a.rec_div[rec * 4 + 2] = uf;
+                a.rec_div[rec * 4 + 3] = ul;
+              }
+            }
+            a.rec_divflag[rec] = flag;
+            if (status == ST_SUCCESS) {
+              mode = M_REFINE;  // x == xacc here
+              rit = 0;
+            } else {
+              for (int v = 0; v < n; ++v) X.st(v, s, XA.ld(v, s));
+              mode = M_FINAL;
+            }
+          }
+        }
+      } else if (mode == M_REFINE) {
+        // endpoint refinement at t = 1: at most 3 iterations, stopping on the update test alone
+        // or on a failed solve (tracker.cpp:446-478); the refined point becomes xacc
+        ++rit;
+        const double dxn = a.sd[D_DXN * a.S + s], xn = a.sd[D_XN * a.S + s];
+        const bool stop = !ok || dxn <= f_mul(a.utol, f_max(1.0, xn));
+        if (stop || rit >= 3) mode = M_FINAL;
+      } else if (mode == M_FINAL) {
+        // final residual ||f(xacc)|| at level R and the certificate (tracker.cpp:480-506)
+        const size_t rec = static_cast<size_t>(path - a.lo);
+        const R resid_r = SR.ldr(R_RESID, s);
+        int st_out = status, rs_out = reason;
+        if (st_out == ST_SUCCESS && rtod(resid_r) > f_mul(10.0, a.rtol)) {
+          st_out = ST_FAILED;
+          rs_out = RS_NOCERT;
+        }
+        for (int v = 0; v < n; ++v) st_flat<R>(a.rec_x + (rec * n + v) * 2 * L, X.ld(v, s));
+#pragma unroll
+        for (int l = 0; l < L; ++l) a.rec_res[rec * L + l] = level<R>::get(resid_r, l);
+        a.rec_status[rec] = static_cast<int8_t>(st_out);
+        a.rec_reason[rec] = static_cast<uint8_t>(rs_out);
+        a.rec_steps[rec] = steps;
+        a.rec_newton[rec] = newton;
+        a.rec_rej[rec] = rej;
+        mode = M_IDLE;
+      }
+
+      if (mode == M_IDLE) {
+        // refill: next start index; seed (tracker.cpp:135-153) and the first prediction
+        path = a.lo + atomicAdd(a.next, 1ull);
+        if (path >= a.hi) {
+          mode = M_DONE;
+        } else {
+          if (a.total_degree) {
+            unsigned long long rem = path;
+            for (int i = n - 1; i >= 0; --i) {
+              const uint32_t d = __ldg(a.degrees + i);
+              const unsigned long long q = rem / d;
+              const uint32_t ri = static_cast<uint32_t>(rem - q * d);
+              rem = q;
+              X.st(i, s, ld_flat<R>(a.roots + (static_cast<size_t>(__ldg(a.root_off + i)) + ri) * 2 * L));
+            }
+          } else {
+            for (int v = 0; v < n; ++v)
+              X.st(v, s, ld_flat<R>(a.explicit_x + (static_cast<size_t>(path - a.lo) * n + v) * 2 * L));
+          }
+          head = 0;
+          len = 1;
+          HT.str(0, s, rfrom<R>(0.0));
+          for (int v = 0; v < n; ++v) {
+            const cx<R> xv = X.ld(v, s);
+            XA.st(v, s, xv);
+            HX.st(v, s, xv);
+          }
+          t = rfrom<R>(0.0);
+          h = rfrom<R>(a.h_init);
+          steps = newton = rej = 0;
+          consec = 0;
+          status = ST_ACTIVE;
+          reason = RS_NONE;
+          predict();
+          mode = M_NEWTON;
+          it = 0;
+          corrected = 0;
+          sing = 0;
+        }
+      }
+
+      a.spath[s] = path;
+      si(F_MODE, s) = mode;
+      si(F_IT, s) = it;
+      si(F_RIT, s) = rit;
+      si(F_LEN, s) = len;
+      si(F_HEAD, s) = head;
+      si(F_CONSEC, s) = consec;
+      si(F_CORR, s) = corrected;
+      si(F_SING, s) = sing;
+      si(F_STATUS, s) = status;
+      si(F_REASON, s) = reason;
+      si(F_STEPS, s) = static_cast<int32_t>(steps);
+      si(F_NEWTON, s) = static_cast<int32_t>(newton);
+      si(F_REJ, s) = static_cast<int32_t>(rej);
+      SR.str(R_T, s, t);
+      SR.str(R_H, s, h);
+      SR.str(R_TNEXT, s, tnext);
+    }
+  }
+  const unsigned busy = __ballot_sync(0xffffffffu, in_range && mode != M_DONE);
+  if ((threadIdx.x & 31) == 0 && busy != 0) atomicAdd(busy_out, static_cast<unsigned>(__popc(busy)));
+}
+
+// ---------------------------------------------------------------------------------------------
+// kernel-level parity entry points
+// ---------------------------------------------------------------------------------------------
+template <class R, int KMAX>
+__global__ void __launch_bounds__(128) eval_kernel(const EvalArgs a) {
+  constexpr int L = level<R>::L;
+  extern __shared__ double smem[];
+  const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= a.batch) return;
+  const int n = a.plan.n;
+  const size_t ls = threadIdx.x;
+  const Planar<R> X{smem, blockDim.x};
+  const Planar<R> JR{smem + static_cast<size_t>(n) * 2 * L * blockDim.x, blockDim.x};
+  const Planar<R> XG{const_cast<double*>(a.x), a.batch}, TG{const_cast<double*>(a.t), a.batch};
+  for (int v = 0; v < n; ++v) X.st(v, ls, XG.ld(v, s));
+  const R t = TG.ldr(0, s);
+  const Planar<R> B{a.sys, a.batch}, J{a.jac, a.batch};
+  double rd;
+  R rr;
+  eval_hj<R, KMAX>(a.plan, X, JR, ls, t, B, J, s, rd, rr);
+  // B holds -H; return H
+  for (int p = 0; p < a.plan.n_polys; ++p) B.st(p, s, cneg(B.ld(p, s)));
+}
+
+template <class R, int NMAX>
+__global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
+  const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= a.batch) return;
+  const Planar<R> Q{a.a, a.batch}, Rm{a.r, a.batch}, B{a.b, a.batch}, Y{a.y, a.batch}, X{a.x, a.batch};
+  cx<R> dx[NMAX];
+  const bool ok = lsq_solve<R, NMAX>(a.n, a.rank_tol, Q, Rm, B, Y, s, dx);
+  a.ok[s] = ok ? 1 : 0;
+#pragma unroll
+  for (int v = 0; v < NMAX; ++v)
+    if (v < a.n) X.st(v, s, ok ? dx[v] : czero<R>());
+}
+
+}  // namespace dev
+}  // namespace pp
+
+// instantiate the three kernels of one (level, NMAX, KMAX) variant
+#define PP_VARIANT(R, NM, KM)                                                         \
+  {NM, KM, reinterpret_cast<const void*>(&pp::dev::eval_trip<R, KM>),                 \
+   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, NM>),                          \
+   reinterpret_cast<const void*>(&pp::dev::step_trip<R>),                             \
+   reinterpret_cast<const void*>(&pp::dev::eval_kernel<R, KM>),                       \
+   reinterpret_cast<const void*>(&pp::dev::lsq_kernel<R, NM>)}
