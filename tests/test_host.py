@@ -1,0 +1,145 @@
+"""Host side of the product (no GPU needed): system grammar, decimal I/O, plan tables, start data,
+gamma, TrackConfig -- each checked bit for bit against the reference build or its golden facts."""
+
+import numpy as np
+import pytest
+
+from conftest import read
+
+
+def need_ref(O):
+    if O.ref is None:
+        pytest.skip("reference build (oracle/_ref) not present")
+
+
+def test_random_gamma_matches_reference(pp, oracle_mod):
+    need_ref(oracle_mod)
+    for seed in (0, 1, 2, 3, 101, 102, 103, 12345, 2**63 + 5):
+        assert pp.random_gamma(seed) == oracle_mod.ref_random_gamma(seed)
+        assert abs(abs(pp.random_gamma(seed)) - 1.0) < 1e-15
+
+
+@pytest.mark.parametrize("text", [
+    "3; x0 + x1 + x2; x0*x1 - 2.5*x2^2; (1.5,-0.25)*x0*x1*x2 - 1;",
+    "2\n# comment\nx0^3 + -x1;\n - 3 - x0*x0*x1 + 0.125e1 ;",
+    "1; x0^2 - 4;",
+    "2; x0*x1 + x1*x0 - 1; 3.14159265358979323846264338327950288419716939937510*x0^7 + x1;",
+])
+def test_parse_print_roundtrip_matches_reference(pp, oracle_mod, text):
+    need_ref(oracle_mod)
+    assert pp.parse_system(text).text() == oracle_mod.ref_print_system(text)
+
+
+@pytest.mark.parametrize("bad", [
+    "0; x0;", "2; x0 + x5;", "1; x0^0;", "1; x0 x0;", "1; 0*x0 + 1;", "1; x0 + 1", "", "1;", "1; x0^-2;",
+    "1; (1,2*x0;",
+])
+def test_parse_errors_raise(pp, bad):
+    with pytest.raises(pp.ParseError):
+        pp.parse_system(bad)
+
+
+def test_cyclic_generator(pp, oracle_mod):
+    need_ref(oracle_mod)
+    for n in (2, 3, 5, 8, 10):
+        assert pp.cyclic_system(n).text() == oracle_mod.ref_cyclic_text(n)
+    s = pp.cyclic_system(10).stats
+    assert (s["dim"], s["n_polys"], s["n_monomials"], s["total_degree"]) == (10, 10, 92, 3628800)
+    with pytest.raises(pp.InvalidArgument):
+        pp.cyclic_system(1)
+
+
+@pytest.mark.parametrize("prec", ["dd", "qd"])
+def test_decimal_parse_and_print_match_reference(pp, oracle_mod, prec):
+    need_ref(oracle_mod)
+    rng = np.random.default_rng(3)
+    samples = ["0", "1", "-0.5", "0.1", "1e-30", "6.02214076e23", "2.718281828459045235360287471352662497757247093699959574966967627",
+               "123456789012345678901234567890.0987654321", "  7.25  "]
+    samples += [f"{rng.uniform(-10, 10):.40f}" for _ in range(50)]
+    for s in samples:
+        a = oracle_mod.ref_parse_decimal(prec, s)
+        b = pp.parse_decimal(prec, s)
+        assert np.array_equal(a, b), s
+        assert oracle_mod.ref_to_decimal(prec, a) == pp.to_decimal(prec, a)
+
+
+@pytest.mark.parametrize("prec", ["d", "dd", "qd"])
+@pytest.mark.parametrize("system", ["cyclic5.sys", "cyclic10.sys"])
+def test_plan_matches_reference(pp, oracle_mod, prec, system):
+    """build_plan (evaldiff.cpp:189-239): same term order, same coefficients bit for bit, same
+    schedule counts (3k-5 position-product multiplications)."""
+    need_ref(oracle_mod)
+    text = read(system)
+    f = pp.parse_system(text)
+    g, _ = pp.total_degree_start(f, prec)
+    gam = pp.random_gamma(1)
+    h = pp.make_homotopy(f, g, gam, prec)
+    ref = oracle_mod.ref_plan(text, prec, pp.gamma_limbs(gam, prec))
+    assert np.array_equal(h.coefficients().reshape(-1), ref["coeff"].reshape(-1))
+    info, rinfo = h.info, oracle_mod.ref_plan_info(text, prec)
+    for k in ("dim", "n_polys", "n_terms", "mon_rows", "posprod_muls", "max_k", "jac_terms", "mon_steps"):
+        assert info[k] == rinfo[k], k
+
+
+def test_plan_geometry_table(pp):
+    """SURVEY.md section 8 geometry: cyclic5/8/10 plan terms, mon rows, steps, cmul steps."""
+    want = {5: (30, 89, 156, 83, 59), 8: (72, 311, 646, 456, 239), 10: (110, 579, 1283, 985, 469)}
+    for n, (terms, rows, steps, cmul, jac) in want.items():
+        f = pp.cyclic_system(n)
+        g, _ = pp.total_degree_start(f, "d")
+        info = pp.make_homotopy(f, g, pp.random_gamma(1), "d").info
+        assert (info["n_terms"], info["mon_rows"], info["mon_steps"], info["cmul_steps"], info["jac_terms"]) == (
+            terms, rows, steps, cmul, jac)
+
+
+@pytest.mark.parametrize("prec", ["d", "dd", "qd"])
+def test_total_degree_starts_match_reference(pp, oracle_mod, prec):
+    need_ref(oracle_mod)
+    text = read("cyclic10.sys")
+    f = pp.parse_system(text)
+    _, st = pp.total_degree_start(f, prec)
+    assert st.count == 3628800
+    for idx in (0, 1, 9, 10, 123456, 2000000, 3628799):
+        assert np.array_equal(st.solution(idx), oracle_mod.ref_td_solution(text, prec, idx, 10))
+
+
+def test_golden_start_pack_equals_total_degree(pp):
+    """cyclic5_starts.txt (reference data) == total_degree_start<QD>(cyclic5) to ~1e-64."""
+    f = pp.parse_system(read("cyclic5.sys"))
+    _, st = pp.total_degree_start(f, "qd")
+    rows = [ln for ln in read("cyclic5_starts.txt").splitlines() if ln.strip()]
+    assert len(rows) == st.count == 120
+    for i in (0, 1, 57, 119):
+        vals = [float(v) for v in rows[i].replace("(", "").replace(")", "").split(",")]
+        sol = st.solution(i)
+        assert np.allclose(sol[:, 0], vals[0::2], atol=1e-15) and np.allclose(sol[:, 4], vals[1::2], atol=1e-15)
+
+
+def test_make_homotopy_checks(pp):
+    f = pp.parse_system("2; x0 + x1; x0*x1 - 1;")
+    g, _ = pp.total_degree_start(f, "dd")
+    with pytest.raises(pp.InvalidArgument):
+        pp.make_homotopy(f, g, 1.5 + 0j, "dd")
+    h3 = pp.parse_system("3; x0; x1; x2;")
+    with pytest.raises(pp.InvalidArgument):
+        pp.make_homotopy(f, h3, 1.0 + 0j, "dd")
+    with pytest.raises(pp.InvalidArgument):
+        pp.total_degree_start(pp.parse_system("2; x0 + x1;"), "d")  # not square
+
+
+def test_track_config_defaults_and_validation(pp, oracle_mod):
+    for prec in ("d", "dd", "qd"):
+        c = pp.TrackConfig.defaults(prec)
+        c.validate()
+        if oracle_mod.ref is not None:
+            r = oracle_mod.ref_defaults(prec)
+            for k, v in r.items():
+                assert getattr(c, k) == v, (prec, k)
+    bad = [dict(h_min=0.2), dict(max_newton=0), dict(batch=0), dict(expand=0.5), dict(contract=1.0),
+           dict(residual_tol=0.0), dict(h_max=0.2), dict(h_init=1e-9)]
+    for kw in bad:
+        c = pp.TrackConfig.defaults("d")
+        for k, v in kw.items():
+            setattr(c, k, v)
+        with pytest.raises(pp.InvalidArgument):
+            c.validate()
