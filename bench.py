@@ -1,0 +1,378 @@
+"""bench.py -- paths/sec to t = 1 of the total-degree homotopy of cyclic 10-roots in complex
+double-double on 1..8 B200 (BASELINE.json metric), against the reference CPU tracker.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--paths B]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+
+A step tracks B start paths of the 3,628,800-path total-degree start set to their terminal status
+(success / failed / diverged after finalize) on every GPU.  Each (step, rank) takes its own
+contiguous chunk of start indices, spread over the index space by a golden-ratio sequence, so N
+GPUs do N times the work (weak scaling) with no data-path collective; the only
+torch.distributed traffic is the barrier and the max-over-ranks timing.
+
+value  = paths / device time of the tracking trips (CUDA events on the library's stream, inputs
+         resident), max over ranks;
+e2e    = paths / wall time of the C-ABI call pp_track_all with host buffers (start tables H2D,
+         all records D2H, host post-processing), max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SYSTEM_FILE = os.path.join(ROOT, "tests", "data", "cyclic10.sys")
+PREC = "dd"
+GAMMA_SEED = 1
+METRIC = "paths/sec to t=1 (cyclic-10, complex dd) at 1/2/4/8 B200 vs host CPU"
+PHI = 0.6180339887498949
+
+
+def chunk_offset(c: int, count: int, B: int) -> int:
+    return int(math.floor(((c + 1) * PHI) % 1.0 * (count - B))) // 64 * 64
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return world, rank, local, dist
+
+
+def barrier(dist, local):
+    if dist is not None:
+        import torch
+
+        torch.cuda.synchronize(local)
+        dist.barrier()
+
+
+def max_over_ranks(dist, local, value: float) -> float:
+    if dist is None:
+        return value
+    import torch
+
+    t = torch.tensor([value], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region"""
+
+    FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active," \
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+                self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        return False
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = max(mx, float(p[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh)
+    return {}
+
+
+def profile_traffic(kernel: str):
+    """dram bytes per launch of `kernel` from the committed ncu summary, if present"""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        d = json.load(fh)
+    return d.get("kernels", {}).get(kernel, {}).get("dram_bytes_per_launch")
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU baseline / reference arm: the reference library (oracle/_ref) on the host cores
+# ------------------------------------------------------------------------------------------------
+def cpu_reference_sample(text: str, count: int, starts: list[tuple[int, int]], threads: int):
+    """track the given [lo, hi) ranges with the reference, one single-worker track_all per thread
+    (the reference's worker pool serialises concurrent callers; per-thread calls do not)"""
+    import oracle as O
+
+    if O.ref is None:
+        raise RuntimeError("oracle/_ref/libppref.so (the reference build) is not present")
+    kind = "reference"
+    gam = complex(*_gamma_pair())
+    results = [None] * len(starts)
+
+    def work(i, lo, hi):
+        results[i] = O.ref_track(text, PREC, gam, lo=lo, hi=hi, workers=1, batch=64)
+
+    pending = list(enumerate(starts))
+    lock = threading.Lock()
+
+    def worker():
+        while True:
+            with lock:
+                if not pending:
+                    return
+                i, (lo, hi) = pending.pop(0)
+            work(i, lo, hi)
+
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=worker) for _ in range(threads)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    wall = time.perf_counter() - t0
+    paths = sum(hi - lo for lo, hi in starts)
+    return paths, wall, kind
+
+
+def _gamma_pair():
+    import paper_1505_00383_b200 as P
+
+    g = P.random_gamma(GAMMA_SEED)
+    return g.real, g.imag
+
+
+def sample_ranges(count: int, B: int, c: int, threads: int, per_thread: int):
+    """per_thread consecutive paths for each thread, spread across chunk c"""
+    off = chunk_offset(c, count, B)
+    stride = max(per_thread, B // threads)
+    return [(off + i * stride, off + i * stride + per_thread) for i in range(threads)]
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return
+    with open(SYSTEM_FILE) as fh:
+        text = fh.read()
+    count = 3628800
+    threads = os.cpu_count() or 1
+    per_thread = args.cpu_paths_per_thread
+    total_paths, total_wall, kind = 0, 0.0, "reference"
+    for s in range(args.warmup + args.steps):
+        rngs = sample_ranges(count, args.paths, s, threads, per_thread)
+        paths, wall, kind = cpu_reference_sample(text, count, rngs, threads)
+        if s >= args.warmup:
+            total_paths += paths
+            total_wall += wall
+    value = total_paths / total_wall
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "paths/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_wall / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "dd (binary64 pairs)",
+        "data": "synthetic: total-degree start solutions of cyclic-10, gamma = random_gamma(1)",
+        "config": {"workload": "cyclic10 total-degree homotopy, complex double-double, TrackConfig::defaults(dd)",
+                   "sample": f"{threads} threads x {per_thread} paths per step (bounded sample of each step's chunk)",
+                   "cpu_threads": threads},
+        "cpu_baseline": {"value": value, "unit": "paths/s", "cores": threads, "kind": kind,
+                         "sample": f"{args.steps} steps x {threads * per_thread} paths, single-worker track_all per thread"},
+        "e2e": {"value": value, "unit": "paths/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------------------
+def fp64_peak_ops(device: int) -> float | None:
+    import paper_1505_00383_b200 as P
+
+    try:
+        return P.fp64_peak(device)
+    except Exception:
+        return None
+
+
+def run_ours(args, world, rank, local, dist):
+    import paper_1505_00383_b200 as P
+    from paper_1505_00383_b200 import work as W
+
+    with open(SYSTEM_FILE) as fh:
+        text = fh.read()
+    f = P.parse_system(text)
+    g, starts = P.total_degree_start(f, PREC)
+    h = P.make_homotopy(f, g, P.random_gamma(GAMMA_SEED), PREC)
+    cfg = P.TrackConfig.defaults(PREC)
+    count = starts.count
+    B = args.paths
+    dim = f.dim
+    records = P.Records(B, dim, PREC)
+    info = h.info
+
+    def step(s):
+        c = s * world + rank
+        lo = chunk_offset(c, count, B)
+        t0 = time.perf_counter()
+        sol = P.track_all(h, starts, cfg, lo=lo, hi=lo + B, device=local, records=records)
+        return sol, time.perf_counter() - t0
+
+    for s in range(args.warmup):
+        step(s)
+    barrier(dist, local)
+    dev_ms, wall_s, launches, paths, conv, h2d, d2h, evals, solves = 0.0, 0.0, 0, 0, 0, 0, 0, 0, 0
+    with ClockSampler(local) as clk:
+        t_all = time.perf_counter()
+        for s in range(args.warmup, args.warmup + args.steps):
+            sol, wall = step(s)
+            st = sol.stats
+            dev_ms += st["device_ms"]
+            wall_s += wall
+            launches += st["kernel_launches"]
+            paths += len(sol)
+            conv += int(np.sum(sol.status == P.SUCCESS))
+            h2d += st["h2d_bytes"]
+            d2h += st["d2h_bytes"]
+            evals += st["evals"]
+            solves += st["solves"]
+        barrier(dist, local)
+        t_all = time.perf_counter() - t_all
+    dev_ms_max = max_over_ranks(dist, local, dev_ms)
+    wall_max = max_over_ranks(dist, local, wall_s)
+    total_paths = paths * world
+    value = total_paths / (dev_ms_max / 1e3)
+    e2e = total_paths / wall_max
+    if rank != 0:
+        return
+
+    # roofline of the dominant kernel: one instrumented step (per-kernel CUDA events)
+    os.environ["PP200_KERNEL_TIMING"] = "1"
+    try:
+        sol_i, _ = step(args.warmup + args.steps)
+    finally:
+        os.environ.pop("PP200_KERNEL_TIMING", None)
+    sti = sol_i.stats
+    work = W.path_work(info, PREC, sti["evals"], sti["solves"])
+    lsq_rate = work["lsq_total"] / (sti["lsq_ms"] / 1e3)
+    eval_rate = work["eval_total"] / (sti["eval_ms"] / 1e3)
+    dominant = "lsq_trip" if sti["lsq_ms"] >= sti["eval_ms"] else "eval_trip"
+    achieved = (lsq_rate if dominant == "lsq_trip" else eval_rate) / 1e12
+    peak_ops = fp64_peak_ops(local)
+    peak = peak_ops / 1e12 if peak_ops else None
+    shares = {k: sti[k] / max(1e-9, sti["eval_ms"] + sti["lsq_ms"] + sti["step_ms"]) for k in ("eval_ms", "lsq_ms", "step_ms")}
+    roofline = {
+        "bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "frac": (achieved / peak) if peak else None,
+        "traffic": profile_traffic(dominant),
+        "kernel": dominant,
+        "op_convention": "binary64 pipe ops (DADD/DMUL/DFMA = 1 each) of the reference arithmetic per Newton iteration",
+        "peak_source": "measured FP64 pipe rate (pp_fp64_peak microbenchmark, this GPU)",
+        "eval_trip_tflops": eval_rate / 1e12, "lsq_trip_tflops": lsq_rate / 1e12,
+        "kernel_time_share": shares,
+        "ops_per_unit": {"eval": work["eval_ops"], "lsq": work["lsq_ops"]},
+        "units": {"evals": sti["evals"], "solves": sti["solves"]},
+        "hbm_bytes_per_iteration": W.bytes_per_iteration(dim, PREC),
+        "hbm_peak_gbs": measured_peaks().get("hbm_gbs"),
+    }
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        rngs = sample_ranges(count, B, args.warmup, threads, args.cpu_paths_per_thread)
+        try:
+            cp, cw, kind = cpu_reference_sample(text, count, rngs, threads)
+            cpu = {"value": cp / cw, "unit": "paths/s", "cores": threads, "kind": kind,
+                   "sample": f"{cp} paths ({threads} threads x {args.cpu_paths_per_thread} consecutive paths "
+                             f"spread over step {args.warmup}'s chunk), single-worker reference track_all per thread"}
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"value": None, "unit": "paths/s", "cores": threads, "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "paths/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "dd (binary64 pairs)",
+        "data": "synthetic: total-degree start solutions of cyclic-10, gamma = random_gamma(1)",
+        "config": {"workload": "cyclic10 total-degree homotopy, complex double-double, TrackConfig::defaults(dd)",
+                   "paths_per_step_per_gpu": B, "chunks": "contiguous start ranges, golden-ratio spread over [0, 3628800)",
+                   "parallelism": f"static path shards x{world}, no collective",
+                   "l2": "working set (slot state, Jacobians) larger than L2 each step", "slots": sol_i.stats["slots"]},
+        "converged_fraction": conv / max(1, paths),
+        "e2e": {"value": e2e, "unit": "paths/s", "h2d_bytes_per_step": h2d // args.steps,
+                "d2h_bytes_per_step": d2h // args.steps},
+        "gpu_launches": launches,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "wall_s": t_all,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--paths", type=int, default=65536, help="start paths per step per GPU")
+    ap.add_argument("--cpu-paths-per-thread", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local, dist = dist_setup()
+    if args.impl == "reference":
+        run_reference_arm(args, world, rank)
+    else:
+        run_ours(args, world, rank, local, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -107,6 +107,11 @@ typedef struct pp_run_stats {
   uint64_t d2h_bytes;
   uint32_t slots;        /* concurrent path slots on the device */
   uint32_t kernel_launches;
+  uint64_t evals;        /* H/Jacobian evaluations performed (corrector + refinement + final) */
+  uint64_t solves;       /* least-squares solves performed (corrector + refinement) */
+  double eval_ms;        /* per-kernel device time; filled only when PP200_KERNEL_TIMING=1 */
+  double lsq_ms;
+  double step_ms;
 } pp_run_stats;
 
 typedef struct pp_system pp_system;     /* PolySystem (polysys.hpp:41-51) */

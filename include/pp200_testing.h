@@ -24,6 +24,8 @@ int pp_test_parse_decimal(int prec, const char* s, double* out);
 int pp_test_to_decimal(int prec, const double* in, char* buf, size_t cap);
 /* per-term (c_start, c_target) coefficient limbs of a homotopy's plan */
 int pp_test_plan_coeffs(const pp_homotopy* h, double* out, size_t cap);
+/* measured FP64 pipe throughput of a device (DFMA ops/s), the roofline denominator */
+int pp_fp64_peak(int device, double* ops_per_s);
 /* [mon_steps, cmul_steps, jac_terms, jac_scaled, n_base] of a homotopy's plan */
 int pp_homotopy_counts(const pp_homotopy* h, uint64_t* counts);
 

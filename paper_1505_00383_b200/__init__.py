@@ -113,6 +113,11 @@ class RunStatsC(ctypes.Structure):
         ("d2h_bytes", ctypes.c_uint64),
         ("slots", ctypes.c_uint32),
         ("kernel_launches", ctypes.c_uint32),
+        ("evals", ctypes.c_uint64),
+        ("solves", ctypes.c_uint64),
+        ("eval_ms", ctypes.c_double),
+        ("lsq_ms", ctypes.c_double),
+        ("step_ms", ctypes.c_double),
     ]
 
 
@@ -158,6 +163,7 @@ _sig("pp_test_arith", _i32, _i32, _i32, _vp, _vp, _vp)
 _sig("pp_test_parse_decimal", _i32, _i32, ctypes.c_char_p, _vp)
 _sig("pp_test_to_decimal", _i32, _i32, _vp, ctypes.c_char_p, _sz)
 _sig("pp_test_plan_coeffs", _i32, _vp, _vp, _sz)
+_sig("pp_fp64_peak", _i32, _i32, _P(_dbl))
 
 EXPORTED = [
     "pp_version", "pp_last_error", "pp_limbs", "pp_system_parse", "pp_system_cyclic", "pp_system_print",
@@ -495,6 +501,13 @@ def lsq_batch(prec, a: np.ndarray, b: np.ndarray, device: int = 0):
     ok = np.zeros(B, dtype=np.uint8)
     _check(lib.pp_lsq_batch(_prec(prec), n, B, _ptr(a), _ptr(b), _ptr(x), _ptr(ok), device))
     return x, ok.astype(bool)
+
+
+def fp64_peak(device: int = 0) -> float:
+    """measured FP64 pipe operations per second of `device` (DFMA microbenchmark)"""
+    v = _dbl()
+    _check(lib.pp_fp64_peak(device, ctypes.byref(v)))
+    return v.value
 
 
 def host_arith(prec, op: int, a, b) -> np.ndarray:

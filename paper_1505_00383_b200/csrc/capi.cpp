@@ -493,6 +493,14 @@ int pp_test_to_decimal(int prec, const double* in, char* buf, size_t cap) {
   return PP_OK;
 }
 
+int pp_fp64_peak(int device, double* ops_per_s) {
+  return guard([&] {
+    need(ops_per_s != nullptr, "pp_fp64_peak: null argument");
+    *ops_per_s = pp::device_fp64_peak(device);
+    return PP_OK;
+  });
+}
+
 // plan coefficients (per term: c_start then c_target, 2L each) for cross-checks against the
 // reference's build_plan
 int pp_test_plan_coeffs(const pp_homotopy* h, double* out, size_t cap) {

@@ -131,6 +131,55 @@ dev::PlanArgs plan_args(const Plan& plan, const DevicePlan* dp) {
 
 bool device_supports(uint32_t n, uint32_t max_k) { return pick_variant(1, n, max_k) != nullptr; }
 
+// ---------------------------------------------------------------------------------------------
+// FP64 pipe throughput microbenchmark: the roofline denominator for the FP64-bound kernels.
+// Eight independent DFMA chains per thread, one resident wave of blocks per SM.
+// ---------------------------------------------------------------------------------------------
+namespace {
+__global__ void fp64_peak_kernel(double* out, int iters) {
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-3, a2 = a0 + 2e-3, a3 = a0 + 3e-3;
+  double a4 = a0 + 4e-3, a5 = a0 + 5e-3, a6 = a0 + 6e-3, a7 = a0 + 7e-3;
+  const double b = 0.999999999, c = 1e-12;
+  for (int i = 0; i < iters; ++i) {
+    a0 = __fma_rn(a0, b, c);
+    a1 = __fma_rn(a1, b, c);
+    a2 = __fma_rn(a2, b, c);
+    a3 = __fma_rn(a3, b, c);
+    a4 = __fma_rn(a4, b, c);
+    a5 = __fma_rn(a5, b, c);
+    a6 = __fma_rn(a6, b, c);
+    a7 = __fma_rn(a7, b, c);
+  }
+  const double s = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+  if (s == 12345.678) out[blockIdx.x] = s;  // keep the chains alive
+}
+}  // namespace
+
+double device_fp64_peak(int device) {
+  DeviceGuard g(device);
+  cudaDeviceProp prop;
+  check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  const int block = 256, per_sm = 8, iters = 1 << 14;
+  const int blocks = prop.multiProcessorCount * per_sm;
+  double* out = dmalloc<double>(blocks);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  fp64_peak_kernel<<<blocks, block>>>(out, iters);  // warm-up
+  cudaEventRecord(e0);
+  const int reps = 5;
+  for (int r = 0; r < reps; ++r) fp64_peak_kernel<<<blocks, block>>>(out, iters);
+  cudaEventRecord(e1);
+  check(cudaEventSynchronize(e1), "fp64 peak kernel");
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  const double ops = static_cast<double>(reps) * blocks * block * iters * 8.0;
+  return ops / (ms / 1e3);
+}
+
 DevicePlan* device_plan_upload(const Plan& plan, int device) {
   DeviceGuard g(device);
   auto* dp = new DevicePlan;
@@ -259,6 +308,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   a.rec_div = cv.take<double>(count * 4);
   a.rec_divflag = cv.take<uint8_t>(count);
   a.next = cv.take<unsigned long long>(8);
+  a.work = a.next + 2;
   unsigned* busy = cv.take<unsigned>(graph_trips);
 
   cudaStream_t stream;
@@ -299,13 +349,44 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   // seeding pass: every slot takes its first path
   check(cudaLaunchKernel(var->step_trip, grid, blk, sargs, 0, stream), "launch step_trip");
 
+  uint64_t trips = 0, launches = 1;
+  float kms[3] = {0, 0, 0};
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  unsigned* h_busy = nullptr;
+  check(cudaMallocHost(&h_busy, sizeof(unsigned)), "cudaMallocHost");
+  if (env_size("PP200_KERNEL_TIMING", 0) != 0) {
+    // instrumented mode: plain launches bracketed by events, per-kernel device time accumulated
+    cudaEvent_t ev[4];
+    for (auto& e : ev) cudaEventCreate(&e);
+    for (;;) {
+      check(cudaMemsetAsync(busy, 0, sizeof(unsigned), stream), "memset busy");
+      void* sa[] = {&a, &busy_slot};
+      cudaEventRecord(ev[0], stream);
+      check(cudaLaunchKernel(var->eval_trip, grid, blk, targs, eval_smem, stream), "launch eval_trip");
+      cudaEventRecord(ev[1], stream);
+      check(cudaLaunchKernel(var->lsq_trip, grid, blk, targs, 0, stream), "launch lsq_trip");
+      cudaEventRecord(ev[2], stream);
+      check(cudaLaunchKernel(var->step_trip, grid, blk, sa, 0, stream), "launch step_trip");
+      cudaEventRecord(ev[3], stream);
+      check(cudaMemcpyAsync(h_busy, busy, sizeof(unsigned), cudaMemcpyDeviceToHost, stream), "D2H");
+      check(cudaStreamSynchronize(stream), "tracker trip");
+      for (int k = 0; k < 3; ++k) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+        kms[k] += ms;
+      }
+      ++trips;
+      launches += 3;
+      if (*h_busy == 0) break;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+  } else {
   // one trip = evaluate, solve, control; trips are captured G at a time into a CUDA graph whose
   // last control kernel reports how many slots are still busy
-  cudaGraph_t graph;
   check(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "capture");
   check(cudaMemsetAsync(busy, 0, graph_trips * sizeof(unsigned), stream), "memset busy");
   std::vector<unsigned*> busy_ptrs(graph_trips);
-  std::vector<void*> step_args(2 * graph_trips);
   for (size_t j = 0; j < graph_trips; ++j) {
     busy_ptrs[j] = busy + j;
     void* sa[] = {&a, &busy_ptrs[j]};
@@ -314,11 +395,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     check(cudaLaunchKernel(var->step_trip, grid, blk, sa, 0, stream), "launch step_trip");
   }
   check(cudaStreamEndCapture(stream, &graph), "end capture");
-  cudaGraphExec_t exec;
   check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
-  unsigned* h_busy = nullptr;
-  check(cudaMallocHost(&h_busy, sizeof(unsigned)), "cudaMallocHost");
-  uint64_t trips = 0, launches = 1;
   for (;;) {
     check(cudaGraphLaunch(exec, stream), "graph launch");
     check(cudaMemcpyAsync(h_busy, busy + graph_trips - 1, sizeof(unsigned), cudaMemcpyDeviceToHost, stream), "D2H");
@@ -327,6 +404,9 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     launches += 3 * graph_trips;
     if (*h_busy == 0) break;
   }
+  }
+  unsigned long long work[2] = {0, 0};
+  check(cudaMemcpyAsync(work, a.work, sizeof work, cudaMemcpyDeviceToHost, stream), "D2H");
   cudaEventRecord(e2, stream);
 
   // records back to the caller's host buffers
@@ -355,8 +435,8 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   cudaEventDestroy(e1);
   cudaEventDestroy(e2);
   cudaEventDestroy(e3);
-  cudaGraphExecDestroy(exec);
-  cudaGraphDestroy(graph);
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
   cudaFreeHost(h_busy);
   cudaStreamDestroy(stream);
 
@@ -384,6 +464,11 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     stats->d2h_bytes = rec_bytes_x + count * (L * 8 + 2 + 12 + 33);
     stats->slots = static_cast<uint32_t>(S);
     stats->kernel_launches = static_cast<uint32_t>(launches);
+    stats->evals = work[0];
+    stats->solves = work[1];
+    stats->eval_ms = kms[0];
+    stats->lsq_ms = kms[1];
+    stats->step_ms = kms[2];
     stats->wall_ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
   }

@@ -36,4 +36,7 @@ inline double default_rank_tol(int prec) { return prec == 0 ? 1e-8 : (prec == 1 
 // largest dimension / monomial support the compiled kernels cover
 bool device_supports(uint32_t n, uint32_t max_k);
 
+// measured FP64 pipe operations per second (DFMA microbenchmark)
+double device_fp64_peak(int device);
+
 }  // namespace pp

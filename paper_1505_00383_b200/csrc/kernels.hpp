@@ -44,6 +44,7 @@ struct TrackArgs {
   // start-index range and refill counter
   unsigned long long lo, hi;
   unsigned long long* next;
+  unsigned long long* work;  // [0] evaluations, [1] least-squares solves issued
   // per-slot storage (S slots).  Planar arrays: element e, limb-plane p, slot s at ((e*P)+p)*S+s.
   size_t S;
   int32_t* si;                  // integer state, field f at f*S + s (track_impl.cuh F_*)

@@ -634,8 +634,14 @@ __global__ void __launch_bounds__(128) step_trip(const TrackArgs a, unsigned* bu
       SR.str(R_TNEXT, s, tnext);
     }
   }
+  // every busy slot has exactly one heavy operation pending for the next trip
   const unsigned busy = __ballot_sync(0xffffffffu, in_range && mode != M_DONE);
-  if ((threadIdx.x & 31) == 0 && busy != 0) atomicAdd(busy_out, static_cast<unsigned>(__popc(busy)));
+  const unsigned solve = __ballot_sync(0xffffffffu, in_range && (mode == M_NEWTON || mode == M_REFINE));
+  if ((threadIdx.x & 31) == 0 && busy != 0) {
+    atomicAdd(busy_out, static_cast<unsigned>(__popc(busy)));
+    atomicAdd(a.work, static_cast<unsigned long long>(__popc(busy)));
+    atomicAdd(a.work + 1, static_cast<unsigned long long>(__popc(solve)));
+  }
 }
 
 // ---------------------------------------------------------------------------------------------

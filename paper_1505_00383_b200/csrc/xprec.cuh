@@ -26,6 +26,14 @@
 #define PP_QD_FN inline
 #endif
 
+// host-only operation counter for the work model (scripts/count_ops.cpp defines PP_COUNT_OPS)
+#if defined(PP_COUNT_OPS) && !defined(__CUDA_ARCH__)
+extern unsigned long long pp_op_count;
+#define PP_COUNT() (++pp_op_count)
+#else
+#define PP_COUNT() ((void)0)
+#endif
+
 namespace pp {
 
 // ---------------------------------------------------------------------------------------------
@@ -35,42 +43,42 @@ PP_HD double f_add(double a, double b) {
 #if defined(__CUDA_ARCH__)
   return __dadd_rn(a, b);
 #else
-  return a + b;
+  PP_COUNT(); return a + b;
 #endif
 }
 PP_HD double f_sub(double a, double b) {
 #if defined(__CUDA_ARCH__)
   return __dsub_rn(a, b);
 #else
-  return a - b;
+  PP_COUNT(); return a - b;
 #endif
 }
 PP_HD double f_mul(double a, double b) {
 #if defined(__CUDA_ARCH__)
   return __dmul_rn(a, b);
 #else
-  return a * b;
+  PP_COUNT(); return a * b;
 #endif
 }
 PP_HD double f_fma(double a, double b, double c) {
 #if defined(__CUDA_ARCH__)
   return __fma_rn(a, b, c);
 #else
-  return std::fma(a, b, c);
+  PP_COUNT(); return std::fma(a, b, c);
 #endif
 }
 PP_HD double f_div(double a, double b) {
 #if defined(__CUDA_ARCH__)
   return __ddiv_rn(a, b);
 #else
-  return a / b;
+  PP_COUNT(); return a / b;
 #endif
 }
 PP_HD double f_sqrt(double a) {
 #if defined(__CUDA_ARCH__)
   return __dsqrt_rn(a);
 #else
-  return std::sqrt(a);
+  PP_COUNT(); return std::sqrt(a);
 #endif
 }
 PP_HD double f_abs(double a) { return std::fabs(a); }

@@ -1,0 +1,25 @@
+"""Short tracking run for ncu: cyclic-10 dd, PATHS start paths at OFFSET (env overrides).
+
+    ncu --set full -k regex:lsq_trip -s 200 -c 1 -o gpurun_out/prof python scripts/profile_run.py
+"""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1505_00383_b200 as P  # noqa: E402
+
+paths = int(os.environ.get("PATHS", "32768"))
+offset = int(os.environ.get("OFFSET", "1000000"))
+prec = os.environ.get("PREC", "dd")
+system = os.environ.get("SYSTEM", "cyclic10.sys")
+root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+f = P.parse_system(open(os.path.join(root, "tests", "data", system)).read())
+g, st = P.total_degree_start(f, prec)
+h = P.make_homotopy(f, g, P.random_gamma(1), prec)
+t0 = time.time()
+sol = P.track_all(h, st, P.TrackConfig.defaults(prec), lo=offset, hi=offset + paths)
+s = sol.stats
+print(f"{system} {prec} {paths} paths: wall {time.time() - t0:.2f}s device {s['device_ms']:.1f} ms trips {s['total_rounds']} "
+      f"evals {s['evals']} solves {s['solves']} eval_ms {s['eval_ms']:.1f} lsq_ms {s['lsq_ms']:.1f} step_ms {s['step_ms']:.1f} "
+      f"-> {paths / (s['device_ms'] / 1e3):.1f} paths/s; {sol.counts()}")

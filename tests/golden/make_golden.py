@@ -81,29 +81,45 @@ def save_lsq(name, prec, n, seed, batch=32):
     print(f"lsq_{name}: {batch} systems, {int(ok.sum())} ok")
 
 
-def main():
+def main(force=False):
     assert O.ref is not None, "build the reference first: make -C oracle ref"
-    c5 = open(os.path.join(DATA, "cyclic5.sys")).read()
-    c10 = open(os.path.join(DATA, "cyclic10.sys")).read()
-    c5g = open(os.path.join(DATA, "cyclic5_start.sys")).read()
-    c5s = open(os.path.join(DATA, "cyclic5_starts.txt")).read()
+    rd = lambda name: open(os.path.join(DATA, name)).read()  # noqa: E731
+    c5, c10, c8 = rd("cyclic5.sys"), rd("cyclic10.sys"), O.ref_cyclic_text(8)
+    k12, r32 = rd("katsura12.sys"), rd("rand32.sys")
+    c5g, c5s = rd("cyclic5_start.sys"), rd("cyclic5_starts.txt")
+    jobs = []
     for prec in ("d", "dd", "qd"):
-        save_eval(f"cyclic5_{prec}", c5, prec, 5)
-        save_eval(f"cyclic10_{prec}", c10, prec, 10)
+        jobs.append((f"eval_cyclic5_{prec}", lambda p=prec: save_eval(f"cyclic5_{p}", c5, p, 5)))
+        jobs.append((f"eval_cyclic10_{prec}", lambda p=prec: save_eval(f"cyclic10_{p}", c10, p, 10)))
         for n in (1, 5, 10, 13):
-            save_lsq(f"n{n}_{prec}", prec, n, 100 + n)
-    save_track("square_d", SQUARE_F, "d", 1, 0, 2, g_text=SQUARE_G, starts_text="1,0\n-1,0\n")
-    save_track("cyclic3_dd", CYC3, "dd", 3, 0, 6)
-    save_track("cyclic5_d", c5, "d", 1, 0, 120)
-    save_track("cyclic5_dd", c5, "dd", 1, 0, 120)
-    save_track("cyclic5_qd", c5, "qd", 1, 0, 8)
-    save_track("cyclic5_dd_seed101", c5, "dd", 101, 0, 120)
-    save_track("cyclic5_file_dd", c5, "dd", 1, 0, 120, g_text=c5g, starts_text=c5s)
-    save_track("cyclic10_d", c10, "d", 1, 0, 512)
-    save_track("cyclic10_dd", c10, "dd", 1, 0, 128)
-    save_track("cyclic10_dd_far", c10, "dd", 1, 1000000, 1000032)
-    save_track("cyclic5_d_tight", c5, "d", 1, 0, 120, cfg={"max_newton": 2, "h_init": 0.1, "max_steps": 40})
+            jobs.append((f"lsq_n{n}_{prec}", lambda p=prec, n=n: save_lsq(f"n{n}_{p}", p, n, 100 + n)))
+    tracks = [
+        ("square_d", SQUARE_F, "d", 1, 0, 2, None, dict(g_text=SQUARE_G, starts_text="1,0\n-1,0\n")),
+        ("cyclic3_dd", CYC3, "dd", 3, 0, 6, None, {}),
+        ("cyclic5_d", c5, "d", 1, 0, 120, None, {}),
+        ("cyclic5_dd", c5, "dd", 1, 0, 120, None, {}),
+        ("cyclic5_qd", c5, "qd", 1, 0, 8, None, {}),
+        ("cyclic5_dd_seed101", c5, "dd", 101, 0, 120, None, {}),
+        ("cyclic5_file_dd", c5, "dd", 1, 0, 120, None, dict(g_text=c5g, starts_text=c5s)),
+        ("cyclic10_d", c10, "d", 1, 0, 512, None, {}),
+        ("cyclic10_dd", c10, "dd", 1, 0, 128, None, {}),
+        ("cyclic10_dd_far", c10, "dd", 1, 1000000, 1000032, None, {}),
+        ("cyclic5_d_tight", c5, "d", 1, 0, 120, {"max_newton": 2, "h_init": 0.1, "max_steps": 40}, {}),
+        ("cyclic8_d", c8, "d", 1, 0, 1024, None, {}),
+        ("cyclic8_dd", c8, "dd", 1, 0, 64, None, {}),
+        ("katsura12_d", k12, "d", 1, 0, 256, None, {}),
+        ("katsura12_dd", k12, "dd", 1, 0, 32, None, {}),
+        ("katsura12_qd_mn4", k12, "qd", 1, 0, 4, {"max_newton": 4}, {}),
+        ("rand32_d", r32, "d", 1, 0, 128, None, {}),
+        ("rand32_dd", r32, "dd", 1, 0, 8, None, {}),
+    ]
+    for name, text, prec, seed, lo, hi, cfg, kw in tracks:
+        jobs.append((f"track_{name}", lambda a=(name, text, prec, seed, lo, hi, cfg, kw):
+                     save_track(a[0], a[1], a[2], a[3], a[4], a[5], cfg=a[6], **a[7])))
+    for fname, job in jobs:
+        if force or not os.path.exists(os.path.join(HERE, fname + ".npz")):
+            job()
 
 
 if __name__ == "__main__":
-    main()
+    main(force="--force" in sys.argv)
