@@ -148,6 +148,10 @@ int pp_load_start_data(const pp_system* g, int prec, const char* text, size_t le
                        double* rejected_resid, uint64_t rejected_cap, uint64_t* n_rejected);
 /* explicit start list, [count][dim][2L] doubles (StartProvenance::file) */
 int pp_starts_explicit(int prec, uint32_t dim, uint64_t count, const double* x, pp_starts** out);
+/* StartData<R> in total-degree mode from its own tables (homotopy.hpp:38-49): degrees[dim] and
+ * the per-variable root tables concatenated, sum(degrees) complex values of 2L doubles.
+ * Index enumeration is StartData::solution's (homotopy.cpp:73-85, last variable fastest). */
+int pp_starts_roots(int prec, uint32_t dim, const uint32_t* degrees, const double* roots, pp_starts** out);
 uint64_t pp_starts_count(const pp_starts* s);
 /* StartData::solution(index) (homotopy.cpp:73-85), dim×2L doubles */
 int pp_starts_solution(const pp_starts* s, uint64_t index, double* x);

@@ -21,7 +21,7 @@ from dataclasses import dataclass, field, fields
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpp200.so")
+LIB_PATH = os.environ.get("PP200_LIB") or os.path.join(_HERE, "libpp200.so")
 
 PRECISIONS = {"d": 0, "dd": 1, "qd": 2}
 LIMBS = {"d": 1, "dd": 2, "qd": 4}
@@ -147,6 +147,7 @@ _sig("pp_random_gamma", None, _u64, _P(_dbl), _P(_dbl))
 _sig("pp_total_degree_start", _i32, _vp, _i32, _P(_vp), _P(_vp))
 _sig("pp_load_start_data", _i32, _vp, _i32, ctypes.c_char_p, _sz, _dbl, _i32, _P(_vp), _vp, _vp, _u64, _P(_u64))
 _sig("pp_starts_explicit", _i32, _i32, _u32, _u64, _vp, _P(_vp))
+_sig("pp_starts_roots", _i32, _i32, _u32, _vp, _vp, _P(_vp))
 _sig("pp_starts_count", _u64, _vp)
 _sig("pp_starts_solution", _i32, _vp, _u64, _vp)
 _sig("pp_starts_free", None, _vp)
@@ -168,7 +169,7 @@ _sig("pp_fp64_peak", _i32, _i32, _P(_dbl))
 EXPORTED = [
     "pp_version", "pp_last_error", "pp_limbs", "pp_system_parse", "pp_system_cyclic", "pp_system_print",
     "pp_system_stats", "pp_system_degrees", "pp_system_free", "pp_random_gamma", "pp_total_degree_start",
-    "pp_load_start_data", "pp_starts_explicit", "pp_starts_count", "pp_starts_solution", "pp_starts_free",
+    "pp_load_start_data", "pp_starts_explicit", "pp_starts_roots", "pp_starts_count", "pp_starts_solution", "pp_starts_free",
     "pp_make_homotopy", "pp_homotopy_info", "pp_homotopy_free", "pp_track_config_defaults",
     "pp_track_config_validate", "pp_track_all", "pp_eval_batch", "pp_lsq_batch",
 ]
@@ -295,6 +296,18 @@ def explicit_starts(x: np.ndarray, prec="dd") -> Starts:
     s = _vp()
     _check(lib.pp_starts_explicit(_prec(prec), dim, count, _ptr(x), ctypes.byref(s)))
     return Starts(s.value, prec, dim)
+
+
+def starts_from_roots(degrees, roots: np.ndarray, prec="dd") -> Starts:
+    """StartData<R> in total-degree mode from its own tables (homotopy.hpp:38-49): degrees[dim]
+    and the per-variable root tables concatenated as [sum(degrees)][2L] limbs."""
+    deg = np.ascontiguousarray(degrees, dtype=np.uint32)
+    r = np.ascontiguousarray(roots, dtype=np.float64)
+    if r.shape[0] != int(deg.sum()):
+        raise InvalidArgument("starts_from_roots: root tables do not match the degrees")
+    s = _vp()
+    _check(lib.pp_starts_roots(_prec(prec), len(deg), _ptr(deg), _ptr(r), ctypes.byref(s)))
+    return Starts(s.value, prec, len(deg))
 
 
 def load_start_data(g: System, text: str, prec="dd", start_tol=1e-8, device=0):

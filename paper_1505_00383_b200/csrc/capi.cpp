@@ -180,6 +180,31 @@ int pp_starts_explicit(int prec, uint32_t dim, uint64_t count, const double* x, 
   });
 }
 
+int pp_starts_roots(int prec, uint32_t dim, const uint32_t* degrees, const double* roots, pp_starts** out) {
+  return guard([&] {
+    const int L = limbs_of(prec);
+    need(L > 0 && out != nullptr && dim > 0 && degrees != nullptr && roots != nullptr,
+         "pp_starts_roots: bad argument");
+    auto so = std::make_unique<pp_starts>();
+    so->st.prec = prec;
+    so->st.L = L;
+    so->st.dim = dim;
+    so->st.total_degree = true;
+    uint64_t count = 1, total = 0;
+    for (uint32_t i = 0; i < dim; ++i) {
+      if (degrees[i] == 0) throw pp::InvalidArgument("pp_starts_roots: zero degree");
+      so->st.degrees.push_back(degrees[i]);
+      so->st.root_off.push_back(static_cast<uint32_t>(total));
+      total += degrees[i];
+      count *= degrees[i];  // as total_degree_start (homotopy.cpp:102)
+    }
+    so->st.count = count;
+    so->st.roots.assign(roots, roots + total * 2 * L);
+    *out = so.release();
+    return PP_OK;
+  });
+}
+
 int pp_load_start_data(const pp_system* g, int prec, const char* text, size_t len, double start_tol,
                        int device, pp_starts** out, uint64_t* rejected_idx, double* rejected_resid,
                        uint64_t rejected_cap, uint64_t* n_rejected) {

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -230,15 +231,40 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
 
   cudaDeviceProp prop;
   check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
-  const size_t eval_smem = static_cast<size_t>(kBlock) * 2 * n * 2 * L * sizeof(double);
-  check(cudaFuncSetAttribute(var->eval_trip, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(eval_smem)),
-        "cudaFuncSetAttribute");
-  // slots: PP200_SLOTS_PER_SM (default 512) per SM, never more than the paths (whole blocks)
-  const size_t per_sm = std::max<size_t>(kBlock, env_size("PP200_SLOTS_PER_SM", 512));
-  uint64_t blocks = (per_sm / kBlock) * static_cast<uint64_t>(prop.multiProcessorCount);
-  blocks = std::min<uint64_t>(blocks, (count + kBlock - 1) / kBlock);
-  blocks = std::max<uint64_t>(blocks, 1);
-  const size_t S = blocks * kBlock;
+  // engine: the trip kernels (default) or the persistent kernel (PP200_ENGINE=fused)
+  const char* eng = std::getenv("PP200_ENGINE");
+  const bool fused = eng != nullptr && std::strcmp(eng, "fused") == 0;
+  const size_t per_thread_smem = static_cast<size_t>(2) * n * 2 * L * sizeof(double);
+  const int tblock = static_cast<int>(std::min<size_t>(128, std::max<size_t>(32, env_size("PP200_TRIP_BLOCK", kBlock))));
+  const size_t eval_smem = static_cast<size_t>(tblock) * per_thread_smem;
+  uint64_t blocks = 0;
+  int fblock = 0;
+  size_t fused_smem = 0;
+  if (fused) {
+    // one resident wave: as many blocks per SM as registers / shared memory allow
+    fblock = static_cast<int>(env_size("PP200_BLOCK", 64));
+    while (fblock > 32 && static_cast<size_t>(fblock) * per_thread_smem > 200 * 1024) fblock /= 2;
+    fused_smem = static_cast<size_t>(fblock) * per_thread_smem;
+    check(cudaFuncSetAttribute(var->fused, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fused_smem)),
+          "cudaFuncSetAttribute");
+    int per_sm = 0;
+    check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var->fused, fblock, fused_smem), "occupancy");
+    if (per_sm < 1) throw CudaFailure("persistent tracker kernel does not fit on an SM");
+    const size_t cap = env_size("PP200_BLOCKS_PER_SM", 0);
+    if (cap) per_sm = std::min<int>(per_sm, static_cast<int>(cap));
+    blocks = static_cast<uint64_t>(per_sm) * prop.multiProcessorCount;
+    blocks = std::min<uint64_t>(blocks, (count + fblock - 1) / fblock);
+    blocks = std::max<uint64_t>(blocks, 1);
+  } else {
+    check(cudaFuncSetAttribute(var->eval_trip, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(eval_smem)),
+          "cudaFuncSetAttribute");
+    // slots: PP200_SLOTS_PER_SM (default 512) per SM, never more than the paths (whole blocks)
+    const size_t per_sm = std::max<size_t>(tblock, env_size("PP200_SLOTS_PER_SM", 512));
+    blocks = (per_sm / tblock) * static_cast<uint64_t>(prop.multiProcessorCount);
+    blocks = std::min<uint64_t>(blocks, (count + tblock - 1) / tblock);
+    blocks = std::max<uint64_t>(blocks, 1);
+  }
+  const size_t S = blocks * (fused ? fblock : tblock);
 
   const size_t cw = 2 * L;  // doubles per complex
   const size_t nJ = static_cast<size_t>(n) * n, nR = static_cast<size_t>(n) * (n + 1) / 2;
@@ -342,23 +368,33 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   check(cudaMemsetAsync(a.si, 0, dev::kIntFields * S * 4, stream), "memset");  // all slots M_IDLE
   check(cudaMemsetAsync(a.next, 0, 8 * sizeof(unsigned long long), stream), "memset");
 
-  const dim3 grid(static_cast<unsigned>(blocks)), blk(kBlock);
+  uint64_t trips = 0, launches = 0;
+  float kms[3] = {0, 0, 0};
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  unsigned* h_busy = nullptr;
+  if (fused) {
+    void* fargs[] = {&a};
+    check(cudaLaunchKernel(var->fused, dim3(static_cast<unsigned>(blocks)), dim3(fblock), fargs, fused_smem, stream),
+          "launch track_fused");
+    launches = 1;
+  } else {
+  const dim3 grid(static_cast<unsigned>(blocks)), blk(tblock);
   void* targs[] = {&a};
   unsigned* busy_slot = busy;
   void* sargs[] = {&a, &busy_slot};
   // seeding pass: every slot takes its first path
   check(cudaLaunchKernel(var->step_trip, grid, blk, sargs, 0, stream), "launch step_trip");
-
-  uint64_t trips = 0, launches = 1;
-  float kms[3] = {0, 0, 0};
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
-  unsigned* h_busy = nullptr;
+  launches = 1;
   check(cudaMallocHost(&h_busy, sizeof(unsigned)), "cudaMallocHost");
   if (env_size("PP200_KERNEL_TIMING", 0) != 0) {
     // instrumented mode: plain launches bracketed by events, per-kernel device time accumulated
     cudaEvent_t ev[4];
     for (auto& e : ev) cudaEventCreate(&e);
+    // PP200_TRIP_LOG=<file>: one line per trip (trip, busy slots, eval/lsq/step ms)
+    const char* log_path = std::getenv("PP200_TRIP_LOG");
+    FILE* trip_log = (log_path && *log_path) ? std::fopen(log_path, "a") : nullptr;
+    unsigned busy_before = static_cast<unsigned>(std::min<uint64_t>(S, count));
     for (;;) {
       check(cudaMemsetAsync(busy, 0, sizeof(unsigned), stream), "memset busy");
       void* sa[] = {&a, &busy_slot};
@@ -371,16 +407,20 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
       cudaEventRecord(ev[3], stream);
       check(cudaMemcpyAsync(h_busy, busy, sizeof(unsigned), cudaMemcpyDeviceToHost, stream), "D2H");
       check(cudaStreamSynchronize(stream), "tracker trip");
+      float tms[3] = {0, 0, 0};
       for (int k = 0; k < 3; ++k) {
-        float ms = 0;
-        cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
-        kms[k] += ms;
+        cudaEventElapsedTime(&tms[k], ev[k], ev[k + 1]);
+        kms[k] += tms[k];
       }
+      if (trip_log) std::fprintf(trip_log, "%llu %u %.4f %.4f %.4f\n", static_cast<unsigned long long>(trips),
+                                 busy_before, tms[0], tms[1], tms[2]);
+      busy_before = *h_busy;
       ++trips;
       launches += 3;
       if (*h_busy == 0) break;
     }
     for (auto& e : ev) cudaEventDestroy(e);
+    if (trip_log) std::fclose(trip_log);
   } else {
   // one trip = evaluate, solve, control; trips are captured G at a time into a CUDA graph whose
   // last control kernel reports how many slots are still busy
@@ -403,6 +443,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     trips += graph_trips;
     launches += 3 * graph_trips;
     if (*h_busy == 0) break;
+  }
   }
   }
   unsigned long long work[2] = {0, 0};
@@ -437,7 +478,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   cudaEventDestroy(e3);
   if (exec) cudaGraphExecDestroy(exec);
   if (graph) cudaGraphDestroy(graph);
-  cudaFreeHost(h_busy);
+  if (h_busy) cudaFreeHost(h_busy);
   cudaStreamDestroy(stream);
 
   // terminal divergence classification: m_est = log(growth) / log(shrink) with the host libm

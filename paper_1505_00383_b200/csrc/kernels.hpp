@@ -92,6 +92,7 @@ struct Variant {
   const void* step_trip;  // __global__ void(TrackArgs, unsigned* busy)
   const void* eval;       // __global__ void(EvalArgs)
   const void* lsq;        // __global__ void(LsqArgs)
+  const void* fused;      // __global__ void(TrackArgs): persistent whole-run kernel
 };
 
 const Variant* variants_d(int* count);

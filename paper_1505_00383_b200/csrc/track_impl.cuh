@@ -27,6 +27,14 @@
 #include "kernels.hpp"
 #include "xprec.cuh"
 
+// register budgets of the trip kernels (minimum resident 128-thread blocks per SM)
+#ifndef PP_LSQ_MINB
+#define PP_LSQ_MINB 3
+#endif
+#ifndef PP_EVAL_MINB
+#define PP_EVAL_MINB 1
+#endif
+
 namespace pp {
 namespace dev {
 
@@ -43,6 +51,14 @@ struct Planar {
   static constexpr int L = level<R>::L;
   double* base;
   size_t S;  // stride between planes (slots, or blockDim for shared memory)
+
+  // an opaque copy: addresses derived from it cannot be hoisted above this point (used at the
+  // top of long loops so loop-invariant per-plane addresses do not pin registers)
+  __device__ __forceinline__ Planar fresh() const {
+    Planar q = *this;
+    asm volatile("" : "+l"(q.base), "+l"(q.S));
+    return q;
+  }
 
   __device__ __forceinline__ cx<R> ld(int e, size_t s) const {
     cx<R> z;
@@ -249,11 +265,16 @@ __device__ void eval_hj(const PlanArgs& pa, const Planar<R>& X, const Planar<R>&
 // Returns false on rank deficiency (r_kk <= rank_tol * max column norm).  The column being
 // orthogonalised is held in registers (NMAX); q_i columns stream from memory.
 template <class R, int NMAX>
-__device__ bool lsq_solve(int n, double rank_tol, const Planar<R>& Q, const Planar<R>& Rm,
-                          const Planar<R>& B, const Planar<R>& Y, size_t s, cx<R> (&dx)[NMAX]) {
+__device__ bool lsq_solve(int n, double rank_tol, const Planar<R>& Q0, const Planar<R>& Rm0,
+                          const Planar<R>& B0, const Planar<R>& Y0, size_t s_in, cx<R> (&dx)[NMAX]) {
+  size_t s = s_in;
+  Planar<R> Q = Q0, Rm = Rm0, B = B0, Y = Y0;
   const cx<R> zero = czero<R>();
   R max_norm = rfrom<R>(0.0);
   for (int j = 0; j < n; ++j) {
+    s = s_in;
+    asm volatile("" : "+l"(s));
+    Q = Q0.fresh();
     R acc = rfrom<R>(0.0);
     for (int r = 0; r < n; ++r) acc = radd(acc, cabs2(Q.ld(j * n + r, s)));
     const R nj = rsqrt(acc);
@@ -262,6 +283,14 @@ __device__ bool lsq_solve(int n, double rank_tol, const Planar<R>& Q, const Plan
   const R tol = rmul(max_norm, rfrom<R>(rank_tol));
 
   for (int k = 0; k < n; ++k) {
+    // per-column laundering of the slot index: no address of this column's loop is hoisted
+    // (keeps the register footprint of the solve independent of the caller's loop nest)
+    s = s_in;
+    asm volatile("" : "+l"(s));
+    Q = Q0.fresh();
+    Rm = Rm0.fresh();
+    B = B0.fresh();
+    Y = Y0.fresh();
     cx<R> ck[NMAX];
 #pragma unroll
     for (int r = 0; r < NMAX; ++r)
@@ -303,6 +332,10 @@ __device__ bool lsq_solve(int n, double rank_tol, const Planar<R>& Q, const Plan
 #pragma unroll
   for (int j = NMAX - 1; j >= 0; --j) {
     if (j < n) {
+      s = s_in;
+      asm volatile("" : "+l"(s));
+      Rm = Rm0.fresh();
+      Y = Y0.fresh();
       cx<R> acc = Y.ld(j, s);
 #pragma unroll
       for (int i = j + 1; i < NMAX; ++i)
@@ -334,7 +367,7 @@ struct SlotInts {
 // trip kernel 1: evaluate H and dH/dx at every busy slot's point
 // ---------------------------------------------------------------------------------------------
 template <class R, int KMAX>
-__global__ void __launch_bounds__(128) eval_trip(const TrackArgs a) {
+__global__ void __launch_bounds__(128, PP_EVAL_MINB) eval_trip(const TrackArgs a) {
   constexpr int L = level<R>::L;
   extern __shared__ double smem[];
   const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -360,7 +393,7 @@ __global__ void __launch_bounds__(128) eval_trip(const TrackArgs a) {
 // trip kernel 2: least-squares Newton update for corrector / refinement slots
 // ---------------------------------------------------------------------------------------------
 template <class R, int NMAX>
-__global__ void __launch_bounds__(128) lsq_trip(const TrackArgs a) {
+__global__ void __launch_bounds__(128, PP_LSQ_MINB) lsq_trip(const TrackArgs a) {
   const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s >= a.S) return;
   const SlotInts si{a.si, a.S};
@@ -388,251 +421,303 @@ __global__ void __launch_bounds__(128) lsq_trip(const TrackArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// trip kernel 3: per-path control -- corrector bookkeeping, step control, status, prediction,
-// finalize and record output, refill from the start counter
+// per-path control: corrector bookkeeping, step control, status, prediction, finalize and record
+// output, refill from the start counter.  Shared by the trip kernels (state in SoA global memory)
+// and the persistent kernel (state in registers).
+// ---------------------------------------------------------------------------------------------
+template <class R>
+struct SlotState {
+  unsigned long long path;
+  int mode, it, rit, len, head, consec, corrected, sing, status, reason;
+  uint32_t steps, newton, rej;
+  R t, h, tnext;
+};
+
+// results of the slot's last heavy operation (evaluation, and least-squares update if any)
+template <class R>
+struct HeavyOut {
+  double resid, dxn, xn;
+  R resid_r;
+  bool ok;
+};
+
+// X: the slot's working point (xs = its column there); every other per-slot array is global at s
+template <class R>
+__device__ __forceinline__ void control(const TrackArgs& a, SlotState<R>& st, const HeavyOut<R>& ho,
+                                        const Planar<R>& X, size_t xs, size_t s) {
+  constexpr int L = level<R>::L;
+  if (st.mode == M_DONE) return;
+  const int n = a.plan.n;
+  const Planar<R> XA{a.xacc, a.S}, HX{a.hx, a.S}, HT{a.ht, a.S};
+  const R one = rfrom<R>(1.0);
+
+  // predictor (tracker.cpp:178-214): t_next = min(t + h, 1); Lagrange extrapolation through
+  // the accepted history (oldest first), a copy when only the start point is known
+  auto predict = [&]() {
+    R tn = radd(st.t, st.h);
+    if (rcmp(tn, one) >= 0) tn = one;
+    st.tnext = tn;
+    const int len = st.len, head = st.head;
+    if (len == 1) {
+      for (int v = 0; v < n; ++v) X.st(v, xs, HX.ld(head * n + v, s));
+      return;
+    }
+    R ts[kHist], w[kHist];
+#pragma unroll
+    for (int i = 0; i < kHist; ++i)
+      if (i < len) ts[i] = HT.ldr((head + i) % kHist, s);
+#pragma unroll
+    for (int i = 0; i < kHist; ++i) {
+      if (i < len) {
+        R wi = one;
+#pragma unroll
+        for (int j = 0; j < kHist; ++j)
+          if (j < len && j != i) wi = rmul(wi, rdiv(rsub(tn, ts[j]), rsub(ts[i], ts[j])));
+        w[i] = wi;
+      }
+    }
+    for (int v = 0; v < n; ++v) {
+      cx<R> acc = czero<R>();
+#pragma unroll
+      for (int i = 0; i < kHist; ++i)
+        if (i < len) acc = cadd(acc, cmulr(HX.ld(((head + i) % kHist) * n + v, s), w[i]));
+      X.st(v, xs, acc);
+    }
+  };
+
+  if (st.mode == M_NEWTON) {
+    ++st.it;
+    ++st.newton;
+    bool done = false;
+    if (!ho.ok) {
+      st.sing = 1;  // this step failed (tracker.cpp:253-257)
+      done = true;
+    } else if (ho.resid <= a.rtol && ho.dxn <= f_mul(a.utol, f_max(1.0, ho.xn))) {
+      st.corrected = 1;
+      done = true;
+    } else if (st.it >= a.max_newton) {
+      done = true;
+    }
+    if (done) {
+      // step control (tracker.cpp:293-317); history push with FIFO drop at depth 5
+      // (tracker.cpp:276-291) kept as a ring buffer
+      double xacc_norm = 0.0;
+      if (st.corrected) {
+        ++st.steps;
+        if (st.consec < 255) ++st.consec;
+        st.t = st.tnext;
+        if (st.len == kHist) {
+          st.head = (st.head + 1) % kHist;
+          st.len = kHist - 1;
+        }
+        const int at = (st.head + st.len) % kHist;
+        HT.str(at, s, st.tnext);
+        for (int v = 0; v < n; ++v) {
+          const cx<R> xv = X.ld(v, xs);
+          XA.st(v, s, xv);
+          HX.st(at * n + v, s, xv);
+        }
+        ++st.len;
+        if (st.consec >= a.expand_after) {
+          const R grown = rmuld(st.h, a.expand);
+          st.h = rcmp(grown, rfrom<R>(a.h_max)) > 0 ? rfrom<R>(a.h_max) : grown;
+        }
+        xacc_norm = ho.xn;  // norm of the accepted point = the last iterate's norm
+      } else {
+        ++st.rej;
+        st.consec = 0;
+        st.h = rmuld(st.h, a.contract);
+        for (int v = 0; v < n; ++v) xacc_norm = f_max(xacc_norm, cabsd(XA.ld(v, s)));
+      }
+      // status on the accepted point (tracker.cpp:319-338)
+      if (xacc_norm > a.div_bound) {
+        st.status = ST_FAILED;
+        st.reason = RS_DIVERGED;
+      } else if (rcmp(st.h, rfrom<R>(a.h_min)) < 0) {
+        st.status = ST_FAILED;
+        st.reason = st.sing ? RS_SINGULAR : RS_UNDERFLOW;
+      } else if (st.steps > a.max_steps) {
+        st.status = ST_FAILED;
+        st.reason = RS_MAXSTEPS;
+      } else if (rcmp(st.t, one) == 0 && st.corrected) {
+        st.status = ST_SUCCESS;
+      }
+
+      if (st.status == ST_ACTIVE) {
+        predict();
+        st.it = 0;
+        st.corrected = 0;
+        st.sing = 0;
+      } else {
+        const size_t rec = static_cast<size_t>(st.path - a.lo);
+        uint8_t flag = 0;
+        if (st.status == ST_FAILED && st.reason != RS_DIVERGED && f_sub(1.0, rtod(st.t)) < 0.01 && st.len >= 3) {
+          // terminal divergence test inputs (tracker.cpp:406-432); the log ratio is taken on
+          // the host with the reference's libm
+          double first = 0.0, prev = -1.0, last = 0.0;
+          bool growing = true;
+          for (int i = 0; i < st.len; ++i) {
+            double nrm = 0.0;
+            const int at = (st.head + i) % kHist;
+            for (int v = 0; v < n; ++v) nrm = f_max(nrm, cabsd(HX.ld(at * n + v, s)));
+            if (nrm <= prev) growing = false;
+            if (i == 0) first = nrm;
+            prev = nrm;
+            last = nrm;
+          }
+          const double uf = f_sub(1.0, rtod(HT.ldr(st.head, s)));
+          const double ul = f_sub(1.0, rtod(HT.ldr((st.head + st.len - 1) % kHist, s)));
+          if (growing && first > 0.0 && ul > 0.0 && uf > ul) {
+            flag = 1;
+            a.rec_div[rec * 4 + 0] = first;
+            a.rec_div[rec * 4 + 1] = last;
+            a.rec_div[rec * 4 + 2] = uf;
+            a.rec_div[rec * 4 + 3] = ul;
+          }
+        }
+        a.rec_divflag[rec] = flag;
+        if (st.status == ST_SUCCESS) {
+          st.mode = M_REFINE;  // x == xacc here
+          st.rit = 0;
+        } else {
+          for (int v = 0; v < n; ++v) X.st(v, xs, XA.ld(v, s));
+          st.mode = M_FINAL;
+        }
+      }
+    }
+  } else if (st.mode == M_REFINE) {
+    // endpoint refinement at t = 1: at most 3 iterations, stopping on the update test alone
+    // or on a failed solve (tracker.cpp:446-478); the refined point becomes xacc
+    ++st.rit;
+    const bool stop = !ho.ok || ho.dxn <= f_mul(a.utol, f_max(1.0, ho.xn));
+    if (stop || st.rit >= 3) st.mode = M_FINAL;
+  } else if (st.mode == M_FINAL) {
+    // final residual ||f(xacc)|| at level R and the certificate (tracker.cpp:480-506)
+    const size_t rec = static_cast<size_t>(st.path - a.lo);
+    int st_out = st.status, rs_out = st.reason;
+    if (st_out == ST_SUCCESS && rtod(ho.resid_r) > f_mul(10.0, a.rtol)) {
+      st_out = ST_FAILED;
+      rs_out = RS_NOCERT;
+    }
+    for (int v = 0; v < n; ++v) st_flat<R>(a.rec_x + (rec * n + v) * 2 * L, X.ld(v, xs));
+#pragma unroll
+    for (int l = 0; l < L; ++l) a.rec_res[rec * L + l] = level<R>::get(ho.resid_r, l);
+    a.rec_status[rec] = static_cast<int8_t>(st_out);
+    a.rec_reason[rec] = static_cast<uint8_t>(rs_out);
+    a.rec_steps[rec] = st.steps;
+    a.rec_newton[rec] = st.newton;
+    a.rec_rej[rec] = st.rej;
+    st.mode = M_IDLE;
+  }
+
+  if (st.mode == M_IDLE) {
+    // refill: next start index; seed (tracker.cpp:135-153) and the first prediction
+    st.path = a.lo + atomicAdd(a.next, 1ull);
+    if (st.path >= a.hi) {
+      st.mode = M_DONE;
+    } else {
+      if (a.total_degree) {
+        unsigned long long rem = st.path;
+        for (int i = n - 1; i >= 0; --i) {
+          const uint32_t d = __ldg(a.degrees + i);
+          const unsigned long long q = rem / d;
+          const uint32_t ri = static_cast<uint32_t>(rem - q * d);
+          rem = q;
+          X.st(i, xs, ld_flat<R>(a.roots + (static_cast<size_t>(__ldg(a.root_off + i)) + ri) * 2 * L));
+        }
+      } else {
+        for (int v = 0; v < n; ++v)
+          X.st(v, xs, ld_flat<R>(a.explicit_x + (static_cast<size_t>(st.path - a.lo) * n + v) * 2 * L));
+      }
+      st.head = 0;
+      st.len = 1;
+      HT.str(0, s, rfrom<R>(0.0));
+      for (int v = 0; v < n; ++v) {
+        const cx<R> xv = X.ld(v, xs);
+        XA.st(v, s, xv);
+        HX.st(v, s, xv);
+      }
+      st.t = rfrom<R>(0.0);
+      st.h = rfrom<R>(a.h_init);
+      st.steps = st.newton = st.rej = 0;
+      st.consec = 0;
+      st.status = ST_ACTIVE;
+      st.reason = RS_NONE;
+      predict();
+      st.mode = M_NEWTON;
+      st.it = 0;
+      st.corrected = 0;
+      st.sing = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// one control step of slot s with its state in the SoA global arrays; returns the new mode
+// ---------------------------------------------------------------------------------------------
+template <class R>
+__device__ __forceinline__ int step_slot(const TrackArgs& a, size_t s, const Planar<R>& X, size_t xs,
+                                         const HeavyOut<R>& ho) {
+  const SlotInts si{a.si, a.S};
+  const Planar<R> SR{a.sr, a.S};
+  SlotState<R> st;
+  st.mode = si(F_MODE, s);
+  if (st.mode == M_DONE) return M_DONE;
+  st.path = a.spath[s];
+  st.it = si(F_IT, s);
+  st.rit = si(F_RIT, s);
+  st.len = si(F_LEN, s);
+  st.head = si(F_HEAD, s);
+  st.consec = si(F_CONSEC, s);
+  st.corrected = si(F_CORR, s);
+  st.sing = si(F_SING, s);
+  st.status = si(F_STATUS, s);
+  st.reason = si(F_REASON, s);
+  st.steps = si(F_STEPS, s);
+  st.newton = si(F_NEWTON, s);
+  st.rej = si(F_REJ, s);
+  st.t = SR.ldr(R_T, s);
+  st.h = SR.ldr(R_H, s);
+  st.tnext = SR.ldr(R_TNEXT, s);
+  control<R>(a, st, ho, X, xs, s);
+  a.spath[s] = st.path;
+  si(F_MODE, s) = st.mode;
+  si(F_IT, s) = st.it;
+  si(F_RIT, s) = st.rit;
+  si(F_LEN, s) = st.len;
+  si(F_HEAD, s) = st.head;
+  si(F_CONSEC, s) = st.consec;
+  si(F_CORR, s) = st.corrected;
+  si(F_SING, s) = st.sing;
+  si(F_STATUS, s) = st.status;
+  si(F_REASON, s) = st.reason;
+  si(F_STEPS, s) = static_cast<int32_t>(st.steps);
+  si(F_NEWTON, s) = static_cast<int32_t>(st.newton);
+  si(F_REJ, s) = static_cast<int32_t>(st.rej);
+  SR.str(R_T, s, st.t);
+  SR.str(R_H, s, st.h);
+  SR.str(R_TNEXT, s, st.tnext);
+  return st.mode;
+}
+
+// ---------------------------------------------------------------------------------------------
+// trip kernel 3: per-path control for every slot
 // ---------------------------------------------------------------------------------------------
 template <class R>
 __global__ void __launch_bounds__(128) step_trip(const TrackArgs a, unsigned* busy_out) {
-  constexpr int L = level<R>::L;
   const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const bool in_range = s < a.S;
   int mode = M_DONE;
   if (in_range) {
     const SlotInts si{a.si, a.S};
-    mode = si(F_MODE, s);
-    if (mode != M_DONE) {
-      const int n = a.plan.n;
-      const Planar<R> X{a.x, a.S}, SR{a.sr, a.S}, XA{a.xacc, a.S}, HX{a.hx, a.S}, HT{a.ht, a.S};
-      const R one = rfrom<R>(1.0);
-      unsigned long long path = a.spath[s];
-      int it = si(F_IT, s), rit = si(F_RIT, s), len = si(F_LEN, s), head = si(F_HEAD, s);
-      int consec = si(F_CONSEC, s), corrected = si(F_CORR, s), sing = si(F_SING, s);
-      int status = si(F_STATUS, s), reason = si(F_REASON, s);
-      uint32_t steps = si(F_STEPS, s), newton = si(F_NEWTON, s), rej = si(F_REJ, s);
-      const bool ok = si(F_OK, s) != 0;
-      R t = SR.ldr(R_T, s), h = SR.ldr(R_H, s), tnext = SR.ldr(R_TNEXT, s);
-
-      // predictor (tracker.cpp:178-214): t_next = min(t + h, 1); Lagrange extrapolation through
-      // the accepted history (oldest first), a copy when only the start point is known
-      auto predict = [&]() {
-        R tn = radd(t, h);
-        if (rcmp(tn, one) >= 0) tn = one;
-        tnext = tn;
-        if (len == 1) {
-          for (int v = 0; v < n; ++v) X.st(v, s, HX.ld(head * n + v, s));
-          return;
-        }
-        R ts[kHist], w[kHist];
-#pragma unroll
-        for (int i = 0; i < kHist; ++i)
-          if (i < len) ts[i] = HT.ldr((head + i) % kHist, s);
-#pragma unroll
-        for (int i = 0; i < kHist; ++i) {
-          if (i < len) {
-            R wi = one;
-#pragma unroll
-            for (int j = 0; j < kHist; ++j)
-              if (j < len && j != i) wi = rmul(wi, rdiv(rsub(tn, ts[j]), rsub(ts[i], ts[j])));
-            w[i] = wi;
-          }
-        }
-        for (int v = 0; v < n; ++v) {
-          cx<R> acc = czero<R>();
-#pragma unroll
-          for (int i = 0; i < kHist; ++i)
-            if (i < len) acc = cadd(acc, cmulr(HX.ld(((head + i) % kHist) * n + v, s), w[i]));
-          X.st(v, s, acc);
-        }
-      };
-
-      if (mode == M_NEWTON) {
-        ++it;
-        ++newton;
-        const double resid = a.sd[D_RESID * a.S + s];
-        const double dxn = a.sd[D_DXN * a.S + s], xn = a.sd[D_XN * a.S + s];
-        bool done = false;
-        if (!ok) {
-          sing = 1;  // this step failed (tracker.cpp:253-257)
-          done = true;
-        } else if (resid <= a.rtol && dxn <= f_mul(a.utol, f_max(1.0, xn))) {
-          corrected = 1;
-          done = true;
-        } else if (it >= a.max_newton) {
-          done = true;
-        }
-        if (done) {
-          // step control (tracker.cpp:293-317); history push with FIFO drop at depth 5
-          // (tracker.cpp:276-291) kept as a ring buffer
-          double xacc_norm = 0.0;
-          if (corrected) {
-            ++steps;
-            if (consec < 255) ++consec;
-            t = tnext;
-            if (len == kHist) {
-              head = (head + 1) % kHist;
-              len = kHist - 1;
-            }
-            const int at = (head + len) % kHist;
-            HT.str(at, s, tnext);
-            for (int v = 0; v < n; ++v) {
-              const cx<R> xv = X.ld(v, s);
-              XA.st(v, s, xv);
-              HX.st(at * n + v, s, xv);
-            }
-            ++len;
-            if (consec >= a.expand_after) {
-              const R grown = rmuld(h, a.expand);
-              h = rcmp(grown, rfrom<R>(a.h_max)) > 0 ? rfrom<R>(a.h_max) : grown;
-            }
-            xacc_norm = xn;  // norm of the accepted point = the last iterate's norm
-          } else {
-            ++rej;
-            consec = 0;
-            h = rmuld(h, a.contract);
-            for (int v = 0; v < n; ++v) xacc_norm = f_max(xacc_norm, cabsd(XA.ld(v, s)));
-          }
-          // status on the accepted point (tracker.cpp:319-338)
-          if (xacc_norm > a.div_bound) {
-            status = ST_FAILED;
-            reason = RS_DIVERGED;
-          } else if (rcmp(h, rfrom<R>(a.h_min)) < 0) {
-            status = ST_FAILED;
-            reason = sing ? RS_SINGULAR : RS_UNDERFLOW;
-          } else if (steps > a.max_steps) {
-            status = ST_FAILED;
-            reason = RS_MAXSTEPS;
-          } else if (rcmp(t, one) == 0 && corrected) {
-            status = ST_SUCCESS;
-          }
-
-          if (status == ST_ACTIVE) {
-            predict();
-            it = 0;
-            corrected = 0;
-            sing = 0;
-          } else {
-            const size_t rec = static_cast<size_t>(path - a.lo);
-            uint8_t flag = 0;
-            if (status == ST_FAILED && reason != RS_DIVERGED && f_sub(1.0, rtod(t)) < 0.01 && len >= 3) {
-              // terminal divergence test inputs (tracker.cpp:406-432); the log ratio is taken on
-              // the host with the reference's libm
-              double first = 0.0, prev = -1.0, last = 0.0;
-              bool growing = true;
-              for (int i = 0; i < len; ++i) {
-                double nrm = 0.0;
-                const int at = (head + i) % kHist;
-                for (int v = 0; v < n; ++v) nrm = f_max(nrm, cabsd(HX.ld(at * n + v, s)));
-                if (nrm <= prev) growing = false;
-                if (i == 0) first = nrm;
-                prev = nrm;
-                last = nrm;
-              }
-              const double uf = f_sub(1.0, rtod(HT.ldr(head, s)));
-              const double ul = f_sub(1.0, rtod(HT.ldr((head + len - 1) % kHist, s)));
-              if (growing && first > 0.0 && ul > 0.0 && uf > ul) {
-                flag = 1;
-                a.rec_div[rec * 4 + 0] = first;
-                a.rec_div[rec * 4 + 1] = last;
-                a.rec_div[rec * 4 + 2] = uf;
-                a.rec_div[rec * 4 + 3] = ul;
-              }
-            }
-            a.rec_divflag[rec] = flag;
-            if (status == ST_SUCCESS) {
-              mode = M_REFINE;  // x == xacc here
-              rit = 0;
-            } else {
-              for (int v = 0; v < n; ++v) X.st(v, s, XA.ld(v, s));
-              mode = M_FINAL;
-            }
-          }
-        }
-      } else if (mode == M_REFINE) {
-        // endpoint refinement at t = 1: at most 3 iterations, stopping on the update test alone
-        // or on a failed solve (tracker.cpp:446-478); the refined point becomes xacc
-        ++rit;
-        const double dxn = a.sd[D_DXN * a.S + s], xn = a.sd[D_XN * a.S + s];
-        const bool stop = !ok || dxn <= f_mul(a.utol, f_max(1.0, xn));
-        if (stop || rit >= 3) mode = M_FINAL;
-      } else if (mode == M_FINAL) {
-        // final residual ||f(xacc)|| at level R and the certificate (tracker.cpp:480-506)
-        const size_t rec = static_cast<size_t>(path - a.lo);
-        const R resid_r = SR.ldr(R_RESID, s);
-        int st_out = status, rs_out = reason;
-        if (st_out == ST_SUCCESS && rtod(resid_r) > f_mul(10.0, a.rtol)) {
-          st_out = ST_FAILED;
-          rs_out = RS_NOCERT;
-        }
-        for (int v = 0; v < n; ++v) st_flat<R>(a.rec_x + (rec * n + v) * 2 * L, X.ld(v, s));
-#pragma unroll
-        for (int l = 0; l < L; ++l) a.rec_res[rec * L + l] = level<R>::get(resid_r, l);
-        a.rec_status[rec] = static_cast<int8_t>(st_out);
-        a.rec_reason[rec] = static_cast<uint8_t>(rs_out);
-        a.rec_steps[rec] = steps;
-        a.rec_newton[rec] = newton;
-        a.rec_rej[rec] = rej;
-        mode = M_IDLE;
-      }
-
-      if (mode == M_IDLE) {
-        // refill: next start index; seed (tracker.cpp:135-153) and the first prediction
-        path = a.lo + atomicAdd(a.next, 1ull);
-        if (path >= a.hi) {
-          mode = M_DONE;
-        } else {
-          if (a.total_degree) {
-            unsigned long long rem = path;
-            for (int i = n - 1; i >= 0; --i) {
-              const uint32_t d = __ldg(a.degrees + i);
-              const unsigned long long q = rem / d;
-              const uint32_t ri = static_cast<uint32_t>(rem - q * d);
-              rem = q;
-              X.st(i, s, ld_flat<R>(a.roots + (static_cast<size_t>(__ldg(a.root_off + i)) + ri) * 2 * L));
-            }
-          } else {
-            for (int v = 0; v < n; ++v)
-              X.st(v, s, ld_flat<R>(a.explicit_x + (static_cast<size_t>(path - a.lo) * n + v) * 2 * L));
-          }
-          head = 0;
-          len = 1;
-          HT.str(0, s, rfrom<R>(0.0));
-          for (int v = 0; v < n; ++v) {
-            const cx<R> xv = X.ld(v, s);
-            XA.st(v, s, xv);
-            HX.st(v, s, xv);
-          }
-          t = rfrom<R>(0.0);
-          h = rfrom<R>(a.h_init);
-          steps = newton = rej = 0;
-          consec = 0;
-          status = ST_ACTIVE;
-          reason = RS_NONE;
-          predict();
-          mode = M_NEWTON;
-          it = 0;
-          corrected = 0;
-          sing = 0;
-        }
-      }
-
-      a.spath[s] = path;
-      si(F_MODE, s) = mode;
-      si(F_IT, s) = it;
-      si(F_RIT, s) = rit;
-      si(F_LEN, s) = len;
-      si(F_HEAD, s) = head;
-      si(F_CONSEC, s) = consec;
-      si(F_CORR, s) = corrected;
-      si(F_SING, s) = sing;
-      si(F_STATUS, s) = status;
-      si(F_REASON, s) = reason;
-      si(F_STEPS, s) = static_cast<int32_t>(steps);
-      si(F_NEWTON, s) = static_cast<int32_t>(newton);
-      si(F_REJ, s) = static_cast<int32_t>(rej);
-      SR.str(R_T, s, t);
-      SR.str(R_H, s, h);
-      SR.str(R_TNEXT, s, tnext);
-    }
+    const Planar<R> X{a.x, a.S}, SR{a.sr, a.S};
+    HeavyOut<R> ho;
+    ho.ok = si(F_OK, s) != 0;
+    ho.resid = a.sd[D_RESID * a.S + s];
+    ho.dxn = a.sd[D_DXN * a.S + s];
+    ho.xn = a.sd[D_XN * a.S + s];
+    ho.resid_r = SR.ldr(R_RESID, s);
+    mode = step_slot<R>(a, s, X, s, ho);
   }
   // every busy slot has exactly one heavy operation pending for the next trip
   const unsigned busy = __ballot_sync(0xffffffffu, in_range && mode != M_DONE);
@@ -642,6 +727,70 @@ __global__ void __launch_bounds__(128) step_trip(const TrackArgs a, unsigned* bu
     atomicAdd(a.work, static_cast<unsigned long long>(__popc(busy)));
     atomicAdd(a.work + 1, static_cast<unsigned long long>(__popc(solve)));
   }
+}
+
+// ---------------------------------------------------------------------------------------------
+// persistent kernel: one launch tracks every path of [lo, hi).  One thread owns one slot for the
+// whole launch and loops {control; heavy operation}; the heavy operation (evaluation, then the
+// least-squares update in corrector / refinement mode) is the same code for every lane of a
+// warp, so lanes run it converged although each is at its own place on its own path.  The
+// working point and the open Jacobian row live in shared memory; the slot state stays in the
+// SoA global arrays (touched once per iteration) so that only the heavy operation's working set
+// occupies registers.  A warp leaves the loop when all its lanes are done.
+// ---------------------------------------------------------------------------------------------
+template <class R, int NMAX, int KMAX>
+__global__ void __launch_bounds__(64) track_fused(const TrackArgs a) {
+  constexpr int L = level<R>::L;
+  extern __shared__ double smem[];
+  const size_t s0 = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // S = grid * block
+  const int n = a.plan.n;
+  const size_t ls0 = threadIdx.x;
+  const Planar<R> J{a.J, a.S}, Rm{a.Rm, a.S}, B{a.B, a.S}, Y{a.Y, a.S};
+
+  HeavyOut<R> ho;
+  ho.resid = ho.dxn = ho.xn = 0.0;
+  ho.resid_r = rfrom<R>(0.0);
+  ho.ok = false;
+  unsigned evals = 0, solves = 0;
+
+  for (;;) {
+    // launder the slot indices once per iteration: keeps the compiler from hoisting the many
+    // loop-invariant per-plane addresses out of the loop (they would pin registers for the
+    // whole launch and force spills in the heavy operation)
+    size_t s = s0, ls = ls0;
+    asm volatile("" : "+l"(s), "+l"(ls));
+    const Planar<R> X{smem, blockDim.x};
+    const Planar<R> JR{smem + static_cast<size_t>(n) * 2 * L * blockDim.x, blockDim.x};
+    const int mode = step_slot<R>(a, s, X, ls, ho);
+    if (__all_sync(0xffffffffu, mode == M_DONE)) break;
+    if (mode == M_NEWTON || mode == M_REFINE || mode == M_FINAL) {
+      const R te = mode == M_NEWTON ? (Planar<R>{a.sr, a.S}.ldr(R_TNEXT, s)) : rfrom<R>(1.0);
+      eval_hj<R, KMAX>(a.plan, X, JR, ls, te, B, J, s, ho.resid, ho.resid_r);
+      ++evals;
+    }
+    if (mode == M_NEWTON || mode == M_REFINE) {
+      cx<R> dx[NMAX];
+      ho.ok = lsq_solve<R, NMAX>(n, a.rank_tol, J, Rm, B, Y, s, dx);
+      ++solves;
+      if (ho.ok) {
+        // x += dx; update and iterate norms (tracker.cpp:258-264)
+        double dxn = 0.0, xn = 0.0;
+#pragma unroll
+        for (int v = 0; v < NMAX; ++v) {
+          if (v < n) {
+            const cx<R> xv = cadd(X.ld(v, ls), dx[v]);
+            X.st(v, ls, xv);
+            dxn = f_max(dxn, cabsd(dx[v]));
+            xn = f_max(xn, cabsd(xv));
+          }
+        }
+        ho.dxn = dxn;
+        ho.xn = xn;
+      }
+    }
+  }
+  atomicAdd(a.work, static_cast<unsigned long long>(evals));
+  atomicAdd(a.work + 1, static_cast<unsigned long long>(solves));
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -690,4 +839,5 @@ __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
    reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, NM>),                          \
    reinterpret_cast<const void*>(&pp::dev::step_trip<R>),                             \
    reinterpret_cast<const void*>(&pp::dev::eval_kernel<R, KM>),                       \
-   reinterpret_cast<const void*>(&pp::dev::lsq_kernel<R, NM>)}
+   reinterpret_cast<const void*>(&pp::dev::lsq_kernel<R, NM>),                       \
+   reinterpret_cast<const void*>(&pp::dev::track_fused<R, NM, KM>)}

@@ -103,6 +103,25 @@ def test_total_degree_starts_match_reference(pp, oracle_mod, prec):
         assert np.array_equal(st.solution(idx), oracle_mod.ref_td_solution(text, prec, idx, 10))
 
 
+@pytest.mark.parametrize("prec", ["d", "dd", "qd"])
+def test_starts_from_root_tables(pp, prec):
+    """pp_starts_roots (the reference StartData's own tables) enumerates exactly as
+    total_degree_start: index -> tuple of roots, last variable fastest (homotopy.cpp:73-85)"""
+    f = pp.parse_system(read("cyclic5.sys"))
+    _, td = pp.total_degree_start(f, prec)
+    deg = f.degrees
+    roots = []
+    for i, d in enumerate(deg):
+        stride = int(np.prod(deg[i + 1:], dtype=np.int64))
+        roots += [td.solution(r * stride)[i] for r in range(d)]
+    st = pp.starts_from_roots(deg, np.array(roots), prec)
+    assert st.count == td.count == 120
+    for i in range(st.count):
+        assert np.array_equal(st.solution(i), td.solution(i))
+    with pytest.raises(pp.InvalidArgument):
+        pp.starts_from_roots([1, 0], np.zeros((1, 2 * pp.LIMBS[prec])), prec)
+
+
 def test_golden_start_pack_equals_total_degree(pp):
     """cyclic5_starts.txt (reference data) == total_degree_start<QD>(cyclic5) to ~1e-64."""
     f = pp.parse_system(read("cyclic5.sys"))
