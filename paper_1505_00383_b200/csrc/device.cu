@@ -156,6 +156,51 @@ __global__ void fp64_peak_kernel(double* out, int iters) {
 }
 }  // namespace
 
+// ---------------------------------------------------------------------------------------------
+// tail compaction (the paper's active-path compaction): once the start counter
+// is exhausted, busy slots above `keep` move into idle slots below it, so the remaining trips
+// launch ceil(keep / block) blocks of densely packed warps.  Slot order does not matter: every
+// per-path result is independent of which slot runs it.
+// ---------------------------------------------------------------------------------------------
+namespace dev {
+namespace {
+__global__ void classify_slots(const MoveArgs m) {
+  const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= m.n_active) return;
+  const bool busy = m.mode[s] != 4;  // M_DONE
+  if (s < m.keep && !busy) m.holes[atomicAdd(m.counts, 1u)] = static_cast<unsigned>(s);
+  if (s >= m.keep && busy) m.movers[atomicAdd(m.counts + 1, 1u)] = static_cast<unsigned>(s);
+}
+__global__ void move_slots(const MoveArgs m) {
+  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m.counts[1]) return;
+  const size_t from = m.movers[i], to = m.holes[i];
+  for (int k = 0; k < m.n_arr; ++k) {
+    const SlotArray& a = m.arr[k];
+    for (int p = 0; p < a.planes; ++p) {
+      const size_t o = static_cast<size_t>(p) * m.S;
+      if (a.bytes == 8) {
+        double* b = static_cast<double*>(a.base);
+        b[o + to] = b[o + from];
+      } else {
+        int32_t* b = static_cast<int32_t*>(a.base);
+        b[o + to] = b[o + from];
+      }
+    }
+  }
+}
+}  // namespace
+
+void launch_compaction(const MoveArgs& m, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  check(cudaMemsetAsync(m.counts, 0, 2 * sizeof(unsigned), st), "memset counts");
+  const unsigned b = 256;
+  classify_slots<<<static_cast<unsigned>((m.n_active + b - 1) / b), b, 0, st>>>(m);
+  move_slots<<<static_cast<unsigned>((m.n_active - m.keep + b - 1) / b + 1), b, 0, st>>>(m);
+  check(cudaGetLastError(), "compaction");
+}
+}  // namespace dev
+
 double device_fp64_peak(int device) {
   DeviceGuard g(device);
   cudaDeviceProp prop;
@@ -231,40 +276,21 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
 
   cudaDeviceProp prop;
   check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
-  // engine: the trip kernels (default) or the persistent kernel (PP200_ENGINE=fused)
-  const char* eng = std::getenv("PP200_ENGINE");
-  const bool fused = eng != nullptr && std::strcmp(eng, "fused") == 0;
   const size_t per_thread_smem = static_cast<size_t>(2) * n * 2 * L * sizeof(double);
-  const int tblock = static_cast<int>(std::min<size_t>(128, std::max<size_t>(32, env_size("PP200_TRIP_BLOCK", kBlock))));
+  int tblock = static_cast<int>(std::min<size_t>(128, std::max<size_t>(32, env_size("PP200_TRIP_BLOCK", kBlock))));
+  while (tblock > 32 && static_cast<size_t>(tblock) * per_thread_smem > 200 * 1024) tblock /= 2;
   const size_t eval_smem = static_cast<size_t>(tblock) * per_thread_smem;
-  uint64_t blocks = 0;
-  int fblock = 0;
-  size_t fused_smem = 0;
-  if (fused) {
-    // one resident wave: as many blocks per SM as registers / shared memory allow
-    fblock = static_cast<int>(env_size("PP200_BLOCK", 64));
-    while (fblock > 32 && static_cast<size_t>(fblock) * per_thread_smem > 200 * 1024) fblock /= 2;
-    fused_smem = static_cast<size_t>(fblock) * per_thread_smem;
-    check(cudaFuncSetAttribute(var->fused, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fused_smem)),
-          "cudaFuncSetAttribute");
-    int per_sm = 0;
-    check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var->fused, fblock, fused_smem), "occupancy");
-    if (per_sm < 1) throw CudaFailure("persistent tracker kernel does not fit on an SM");
-    const size_t cap = env_size("PP200_BLOCKS_PER_SM", 0);
-    if (cap) per_sm = std::min<int>(per_sm, static_cast<int>(cap));
-    blocks = static_cast<uint64_t>(per_sm) * prop.multiProcessorCount;
-    blocks = std::min<uint64_t>(blocks, (count + fblock - 1) / fblock);
-    blocks = std::max<uint64_t>(blocks, 1);
-  } else {
-    check(cudaFuncSetAttribute(var->eval_trip, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(eval_smem)),
-          "cudaFuncSetAttribute");
-    // slots: PP200_SLOTS_PER_SM (default 512) per SM, never more than the paths (whole blocks)
-    const size_t per_sm = std::max<size_t>(tblock, env_size("PP200_SLOTS_PER_SM", 512));
-    blocks = (per_sm / tblock) * static_cast<uint64_t>(prop.multiProcessorCount);
-    blocks = std::min<uint64_t>(blocks, (count + tblock - 1) / tblock);
-    blocks = std::max<uint64_t>(blocks, 1);
-  }
-  const size_t S = blocks * (fused ? fblock : tblock);
+  const size_t lsq_smem = eval_smem / 2;  // the column being orthogonalised
+  check(cudaFuncSetAttribute(var->eval_trip, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(eval_smem)),
+        "cudaFuncSetAttribute");
+  check(cudaFuncSetAttribute(var->lsq_trip, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsq_smem)),
+        "cudaFuncSetAttribute");
+  // slots: PP200_SLOTS_PER_SM (default 512) per SM, never more than the paths (whole blocks)
+  const size_t per_sm = std::max<size_t>(tblock, env_size("PP200_SLOTS_PER_SM", 512));
+  uint64_t blocks = (per_sm / tblock) * static_cast<uint64_t>(prop.multiProcessorCount);
+  blocks = std::min<uint64_t>(blocks, (count + tblock - 1) / tblock);
+  blocks = std::max<uint64_t>(blocks, 1);
+  const size_t S = blocks * tblock;
 
   const size_t cw = 2 * L;  // doubles per complex
   const size_t nJ = static_cast<size_t>(n) * n, nR = static_cast<size_t>(n) * (n + 1) / 2;
@@ -368,83 +394,130 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   check(cudaMemsetAsync(a.si, 0, dev::kIntFields * S * 4, stream), "memset");  // all slots M_IDLE
   check(cudaMemsetAsync(a.next, 0, 8 * sizeof(unsigned long long), stream), "memset");
 
-  uint64_t trips = 0, launches = 0;
+  uint64_t trips = 0, launches = 0, compactions = 0;
   float kms[3] = {0, 0, 0};
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
-  unsigned* h_busy = nullptr;
-  if (fused) {
-    void* fargs[] = {&a};
-    check(cudaLaunchKernel(var->fused, dim3(static_cast<unsigned>(blocks)), dim3(fblock), fargs, fused_smem, stream),
-          "launch track_fused");
+  // pinned mailbox: [0] busy slots after the last control kernel, [1] start counter
+  unsigned long long* mbox = nullptr;
+  check(cudaMallocHost(&mbox, 2 * sizeof(unsigned long long)), "cudaMallocHost");
+  a.n_active = S;
+  {
+    const dim3 blk(tblock);
+    dim3 grid(static_cast<unsigned>(blocks));
+    void* targs[] = {&a};
+    unsigned* busy_slot = busy;
+    void* sargs[] = {&a, &busy_slot};
+    // seeding pass: every slot takes its first path
+    check(cudaLaunchKernel(var->step_trip, grid, blk, sargs, 0, stream), "launch step_trip");
     launches = 1;
-  } else {
-  const dim3 grid(static_cast<unsigned>(blocks)), blk(tblock);
-  void* targs[] = {&a};
-  unsigned* busy_slot = busy;
-  void* sargs[] = {&a, &busy_slot};
-  // seeding pass: every slot takes its first path
-  check(cudaLaunchKernel(var->step_trip, grid, blk, sargs, 0, stream), "launch step_trip");
-  launches = 1;
-  check(cudaMallocHost(&h_busy, sizeof(unsigned)), "cudaMallocHost");
-  if (env_size("PP200_KERNEL_TIMING", 0) != 0) {
-    // instrumented mode: plain launches bracketed by events, per-kernel device time accumulated
-    cudaEvent_t ev[4];
-    for (auto& e : ev) cudaEventCreate(&e);
-    // PP200_TRIP_LOG=<file>: one line per trip (trip, busy slots, eval/lsq/step ms)
-    const char* log_path = std::getenv("PP200_TRIP_LOG");
-    FILE* trip_log = (log_path && *log_path) ? std::fopen(log_path, "a") : nullptr;
-    unsigned busy_before = static_cast<unsigned>(std::min<uint64_t>(S, count));
-    for (;;) {
-      check(cudaMemsetAsync(busy, 0, sizeof(unsigned), stream), "memset busy");
-      void* sa[] = {&a, &busy_slot};
-      cudaEventRecord(ev[0], stream);
-      check(cudaLaunchKernel(var->eval_trip, grid, blk, targs, eval_smem, stream), "launch eval_trip");
-      cudaEventRecord(ev[1], stream);
-      check(cudaLaunchKernel(var->lsq_trip, grid, blk, targs, 0, stream), "launch lsq_trip");
-      cudaEventRecord(ev[2], stream);
-      check(cudaLaunchKernel(var->step_trip, grid, blk, sa, 0, stream), "launch step_trip");
-      cudaEventRecord(ev[3], stream);
-      check(cudaMemcpyAsync(h_busy, busy, sizeof(unsigned), cudaMemcpyDeviceToHost, stream), "D2H");
-      check(cudaStreamSynchronize(stream), "tracker trip");
-      float tms[3] = {0, 0, 0};
-      for (int k = 0; k < 3; ++k) {
-        cudaEventElapsedTime(&tms[k], ev[k], ev[k + 1]);
-        kms[k] += tms[k];
+
+    // tail compaction once the start counter is exhausted and at most half the launched slots
+    // are busy (PP200_COMPACT=0 disables it)
+    const bool compact = env_size("PP200_COMPACT", 1) != 0;
+    unsigned* holes = nullptr;
+    if (compact) check(cudaMallocAsync(reinterpret_cast<void**>(&holes), (2 * S + 2) * sizeof(unsigned), stream), "alloc");
+    auto maybe_compact = [&](unsigned long long nbusy, unsigned long long started) -> bool {
+      if (!compact || started < count || nbusy == 0 || nbusy * 2 > a.n_active) return false;
+      const size_t keep = (nbusy + tblock - 1) / tblock * tblock;
+      if (keep >= a.n_active) return false;
+      dev::MoveArgs m{};
+      const size_t nL = n * cw;
+      const dev::SlotArray arrs[] = {
+          {a.si, dev::kIntFields, 4}, {a.spath, 1, 8}, {a.sr, dev::kRealFields * static_cast<int>(L), 8},
+          {a.sd, dev::kDblFields, 8}, {a.x, static_cast<int>(nL), 8}, {a.xacc, static_cast<int>(nL), 8},
+          {a.hx, static_cast<int>(kH * nL), 8}, {a.ht, static_cast<int>(kH * L), 8}};
+      m.n_arr = static_cast<int>(sizeof(arrs) / sizeof(arrs[0]));
+      for (int i = 0; i < m.n_arr; ++i) m.arr[i] = arrs[i];
+      m.S = S;
+      m.n_active = a.n_active;
+      m.keep = keep;
+      m.mode = a.si;  // plane F_MODE = 0
+      m.holes = holes;
+      m.movers = holes + S;
+      m.counts = holes + 2 * S;
+      dev::launch_compaction(m, stream);
+      a.n_active = keep;
+      grid = dim3(static_cast<unsigned>(keep / tblock));
+      ++compactions;
+      launches += 2;
+      return true;
+    };
+
+    if (env_size("PP200_KERNEL_TIMING", 0) != 0) {
+      // instrumented mode: plain launches bracketed by events, per-kernel device time accumulated
+      cudaEvent_t ev[4];
+      for (auto& e : ev) cudaEventCreate(&e);
+      // PP200_TRIP_LOG=<file>: one line per trip (trip, busy slots, eval/lsq/step ms)
+      const char* log_path = std::getenv("PP200_TRIP_LOG");
+      FILE* trip_log = (log_path && *log_path) ? std::fopen(log_path, "a") : nullptr;
+      unsigned long long busy_before = std::min<uint64_t>(S, count);
+      for (;;) {
+        check(cudaMemsetAsync(busy, 0, sizeof(unsigned), stream), "memset busy");
+        void* sa[] = {&a, &busy_slot};
+        cudaEventRecord(ev[0], stream);
+        check(cudaLaunchKernel(var->eval_trip, grid, blk, targs, eval_smem, stream), "launch eval_trip");
+        cudaEventRecord(ev[1], stream);
+        check(cudaLaunchKernel(var->lsq_trip, grid, blk, targs, lsq_smem, stream), "launch lsq_trip");
+        cudaEventRecord(ev[2], stream);
+        check(cudaLaunchKernel(var->step_trip, grid, blk, sa, 0, stream), "launch step_trip");
+        cudaEventRecord(ev[3], stream);
+        check(cudaMemcpyAsync(mbox, busy, sizeof(unsigned), cudaMemcpyDeviceToHost, stream), "D2H");
+        check(cudaMemcpyAsync(mbox + 1, a.next, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream), "D2H");
+        check(cudaStreamSynchronize(stream), "tracker trip");
+        const unsigned long long nbusy = *reinterpret_cast<unsigned*>(mbox);
+        float tms[3] = {0, 0, 0};
+        for (int k = 0; k < 3; ++k) {
+          cudaEventElapsedTime(&tms[k], ev[k], ev[k + 1]);
+          kms[k] += tms[k];
+        }
+        if (trip_log)
+          std::fprintf(trip_log, "%llu %llu %.4f %.4f %.4f %llu\n", static_cast<unsigned long long>(trips), busy_before,
+                       tms[0], tms[1], tms[2], static_cast<unsigned long long>(a.n_active));
+        busy_before = nbusy;
+        ++trips;
+        launches += 3;
+        if (nbusy == 0) break;
+        maybe_compact(nbusy, mbox[1]);
       }
-      if (trip_log) std::fprintf(trip_log, "%llu %u %.4f %.4f %.4f\n", static_cast<unsigned long long>(trips),
-                                 busy_before, tms[0], tms[1], tms[2]);
-      busy_before = *h_busy;
-      ++trips;
-      launches += 3;
-      if (*h_busy == 0) break;
+      for (auto& e : ev) cudaEventDestroy(e);
+      if (trip_log) std::fclose(trip_log);
+    } else {
+      // one trip = evaluate, solve, control; trips are captured G at a time into a CUDA graph
+      // whose last control kernel reports how many slots are still busy.  The graph is
+      // re-captured when compaction shrinks the launch.
+      auto capture = [&]() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        exec = nullptr;
+        graph = nullptr;
+        check(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "capture");
+        check(cudaMemsetAsync(busy, 0, graph_trips * sizeof(unsigned), stream), "memset busy");
+        std::vector<unsigned*> busy_ptrs(graph_trips);
+        for (size_t j = 0; j < graph_trips; ++j) {
+          busy_ptrs[j] = busy + j;
+          void* sa[] = {&a, &busy_ptrs[j]};
+          check(cudaLaunchKernel(var->eval_trip, grid, blk, targs, eval_smem, stream), "launch eval_trip");
+          check(cudaLaunchKernel(var->lsq_trip, grid, blk, targs, lsq_smem, stream), "launch lsq_trip");
+          check(cudaLaunchKernel(var->step_trip, grid, blk, sa, 0, stream), "launch step_trip");
+        }
+        check(cudaStreamEndCapture(stream, &graph), "end capture");
+        check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
+      };
+      capture();
+      for (;;) {
+        check(cudaGraphLaunch(exec, stream), "graph launch");
+        check(cudaMemcpyAsync(mbox, busy + graph_trips - 1, sizeof(unsigned), cudaMemcpyDeviceToHost, stream), "D2H");
+        check(cudaMemcpyAsync(mbox + 1, a.next, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream), "D2H");
+        check(cudaStreamSynchronize(stream), "tracker trips");
+        trips += graph_trips;
+        launches += 3 * graph_trips;
+        const unsigned long long nbusy = *reinterpret_cast<unsigned*>(mbox);
+        if (nbusy == 0) break;
+        if (maybe_compact(nbusy, mbox[1])) capture();
+      }
     }
-    for (auto& e : ev) cudaEventDestroy(e);
-    if (trip_log) std::fclose(trip_log);
-  } else {
-  // one trip = evaluate, solve, control; trips are captured G at a time into a CUDA graph whose
-  // last control kernel reports how many slots are still busy
-  check(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "capture");
-  check(cudaMemsetAsync(busy, 0, graph_trips * sizeof(unsigned), stream), "memset busy");
-  std::vector<unsigned*> busy_ptrs(graph_trips);
-  for (size_t j = 0; j < graph_trips; ++j) {
-    busy_ptrs[j] = busy + j;
-    void* sa[] = {&a, &busy_ptrs[j]};
-    check(cudaLaunchKernel(var->eval_trip, grid, blk, targs, eval_smem, stream), "launch eval_trip");
-    check(cudaLaunchKernel(var->lsq_trip, grid, blk, targs, 0, stream), "launch lsq_trip");
-    check(cudaLaunchKernel(var->step_trip, grid, blk, sa, 0, stream), "launch step_trip");
-  }
-  check(cudaStreamEndCapture(stream, &graph), "end capture");
-  check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
-  for (;;) {
-    check(cudaGraphLaunch(exec, stream), "graph launch");
-    check(cudaMemcpyAsync(h_busy, busy + graph_trips - 1, sizeof(unsigned), cudaMemcpyDeviceToHost, stream), "D2H");
-    check(cudaStreamSynchronize(stream), "tracker trips");
-    trips += graph_trips;
-    launches += 3 * graph_trips;
-    if (*h_busy == 0) break;
-  }
-  }
+    if (holes) cudaFreeAsync(holes, stream);
   }
   unsigned long long work[2] = {0, 0};
   check(cudaMemcpyAsync(work, a.work, sizeof work, cudaMemcpyDeviceToHost, stream), "D2H");
@@ -478,7 +551,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   cudaEventDestroy(e3);
   if (exec) cudaGraphExecDestroy(exec);
   if (graph) cudaGraphDestroy(graph);
-  if (h_busy) cudaFreeHost(h_busy);
+  cudaFreeHost(mbox);
   cudaStreamDestroy(stream);
 
   // terminal divergence classification: m_est = log(growth) / log(shrink) with the host libm
@@ -553,7 +626,8 @@ void device_eval(const Plan& plan, DevicePlan* dp, uint32_t batch, const double*
   a.t = dt;
   a.sys = ds;
   a.jac = dj;
-  const int block = 128;
+  int block = 128;
+  while (block > 32 && static_cast<size_t>(block) * 2 * n * w * sizeof(double) > 200 * 1024) block /= 2;
   const size_t smem = static_cast<size_t>(block) * 2 * n * w * sizeof(double);
   check(cudaFuncSetAttribute(var->eval, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)), "attr");
   void* args[] = {&a};
@@ -595,8 +669,11 @@ void device_lsq(int prec, uint32_t n, uint32_t batch, const double* a, const dou
   uint8_t* dok = dmalloc<uint8_t>(batch);
   dev::LsqArgs args{static_cast<int>(n), batch, default_rank_tol(prec), da, dr, db, dy, dxv, dok};
   void* pa[] = {&args};
-  const int block = 128;
-  check(cudaLaunchKernel(var->lsq, dim3((batch + block - 1) / block), dim3(block), pa, 0, 0), "launch lsq");
+  int block = 128;
+  while (block > 32 && static_cast<size_t>(block) * n * w * sizeof(double) > 200 * 1024) block /= 2;
+  const size_t smem = static_cast<size_t>(block) * n * w * sizeof(double);
+  check(cudaFuncSetAttribute(var->lsq, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)), "attr");
+  check(cudaLaunchKernel(var->lsq, dim3((batch + block - 1) / block), dim3(block), pa, smem, 0), "launch lsq");
   check(cudaDeviceSynchronize(), "lsq kernel");
   std::vector<double> hx(static_cast<size_t>(batch) * n * w);
   check(cudaMemcpy(hx.data(), dxv, hx.size() * 8, cudaMemcpyDeviceToHost), "D2H");

@@ -46,7 +46,8 @@ struct TrackArgs {
   unsigned long long* next;
   unsigned long long* work;  // [0] evaluations, [1] least-squares solves issued
   // per-slot storage (S slots).  Planar arrays: element e, limb-plane p, slot s at ((e*P)+p)*S+s.
-  size_t S;
+  size_t S;         // slot stride of the planar arrays
+  size_t n_active;  // slots [0, n_active) are launched (shrinks when the tail is compacted)
   int32_t* si;                  // integer state, field f at f*S + s (track_impl.cuh F_*)
   unsigned long long* spath;    // start index owned by the slot
   double* sr;                   // level-R scalars (t, h, t_next, final residual), planar real
@@ -92,8 +93,25 @@ struct Variant {
   const void* step_trip;  // __global__ void(TrackArgs, unsigned* busy)
   const void* eval;       // __global__ void(EvalArgs)
   const void* lsq;        // __global__ void(LsqArgs)
-  const void* fused;      // __global__ void(TrackArgs): persistent whole-run kernel
 };
+
+// tail compaction: move the busy slots of [keep, n_active) into idle slots of [0, keep)
+struct SlotArray {
+  void* base;   // planar, plane p of slot s at base + (p*S + s) * bytes
+  int planes;
+  int bytes;    // 4 or 8
+};
+constexpr int kMaxSlotArrays = 12;
+struct MoveArgs {
+  SlotArray arr[kMaxSlotArrays];
+  int n_arr;
+  size_t S, n_active, keep;
+  const int32_t* mode;  // plane F_MODE of the integer state
+  unsigned* holes;      // idle slots below keep
+  unsigned* movers;     // busy slots at or above keep
+  unsigned* counts;     // [0] holes, [1] movers
+};
+void launch_compaction(const MoveArgs& m, void* stream);
 
 const Variant* variants_d(int* count);
 const Variant* variants_dd(int* count);

@@ -258,24 +258,38 @@ __device__ void eval_hj(const PlanArgs& pa, const Planar<R>& X, const Planar<R>&
 }
 
 // ---------------------------------------------------------------------------------------------
-// least squares by two-pass modified Gram-Schmidt (reference linalg.hpp:79-125)
+// least squares, shared-memory column variant (the one the tracker runs)
 // ---------------------------------------------------------------------------------------------
-// Q: n x n column-major (element col*n + row), overwritten by the orthonormal factor;
-// Rm: packed upper triangle (element i + k(k+1)/2); B: right-hand side; Y: scratch (Q^H b).
-// Returns false on rank deficiency (r_kk <= rank_tol * max column norm).  The column being
-// orthogonalised is held in registers (NMAX); q_i columns stream from memory.
-template <class R, int NMAX>
-__device__ bool lsq_solve(int n, double rank_tol, const Planar<R>& Q0, const Planar<R>& Rm0,
-                          const Planar<R>& B0, const Planar<R>& Y0, size_t s_in, cx<R> (&dx)[NMAX]) {
-  size_t s = s_in;
-  Planar<R> Q = Q0, Rm = Rm0, B = B0, Y = Y0;
+// Same operation sequence as lsq_solve (linalg.hpp:79-125), but the column being
+// orthogonalised lives in shared memory (C, this thread's column cs), so every row loop is a
+// short rolled loop: the solve needs few registers (high occupancy) and its code stays resident
+// in the instruction cache.  While column q_i is being applied, the next column to be read is
+// prefetched into L1.  On success dx is left in C (elements 0..n-1).
+#ifndef PP_LSQ_UNROLL
+#define PP_LSQ_UNROLL 2
+#endif
+#define PP_STR_(x) #x
+#define PP_STR(x) PP_STR_(x)
+#define PP_UNROLL_ROWS _Pragma(PP_STR(unroll PP_LSQ_UNROLL))
+
+__device__ __forceinline__ void prefetch_l1(const double* p) { asm volatile("prefetch.L1 [%0];" ::"l"(p)); }
+
+template <class R>
+__device__ __forceinline__ void prefetch_column(const Planar<R>& Q, int col, int n, size_t s) {
+  constexpr int L = level<R>::L;
+  const double* p = Q.base + static_cast<size_t>(col) * n * 2 * L * Q.S + s;
+  for (int e = 0; e < n * 2 * L; ++e) prefetch_l1(p + static_cast<size_t>(e) * Q.S);
+}
+
+template <class R>
+__device__ bool lsq_solve_c(int n, double rank_tol, const Planar<R>& Q, const Planar<R>& Rm,
+                            const Planar<R>& B, const Planar<R>& Y, size_t s, const Planar<R>& C,
+                            size_t cs) {
   const cx<R> zero = czero<R>();
   R max_norm = rfrom<R>(0.0);
   for (int j = 0; j < n; ++j) {
-    s = s_in;
-    asm volatile("" : "+l"(s));
-    Q = Q0.fresh();
     R acc = rfrom<R>(0.0);
+PP_UNROLL_ROWS
     for (int r = 0; r < n; ++r) acc = radd(acc, cabs2(Q.ld(j * n + r, s)));
     const R nj = rsqrt(acc);
     if (rcmp(nj, max_norm) > 0) max_norm = nj;
@@ -283,65 +297,44 @@ __device__ bool lsq_solve(int n, double rank_tol, const Planar<R>& Q0, const Pla
   const R tol = rmul(max_norm, rfrom<R>(rank_tol));
 
   for (int k = 0; k < n; ++k) {
-    // per-column laundering of the slot index: no address of this column's loop is hoisted
-    // (keeps the register footprint of the solve independent of the caller's loop nest)
-    s = s_in;
-    asm volatile("" : "+l"(s));
-    Q = Q0.fresh();
-    Rm = Rm0.fresh();
-    B = B0.fresh();
-    Y = Y0.fresh();
-    cx<R> ck[NMAX];
-#pragma unroll
-    for (int r = 0; r < NMAX; ++r)
-      if (r < n) ck[r] = Q.ld(k * n + r, s);
+PP_UNROLL_ROWS
+    for (int r = 0; r < n; ++r) C.st(r, cs, Q.ld(k * n + r, s));
     const int rk = k * (k + 1) / 2;
     for (int pass = 0; pass < 2; ++pass) {
       for (int i = 0; i < k; ++i) {
+        // next column read: q_(i+1), else q_0 of the second pass, else the next column
+        const int nxt = i + 1 < k ? i + 1 : (pass == 0 ? 0 : k + 1);
+        if (nxt < n) prefetch_column<R>(Q, nxt, n, s);
         cx<R> rik = zero;
-#pragma unroll
-        for (int r = 0; r < NMAX; ++r)
-          if (r < n) rik = cadd(rik, cmul(cconj(Q.ld(i * n + r, s)), ck[r]));
+PP_UNROLL_ROWS
+        for (int r = 0; r < n; ++r) rik = cadd(rik, cmul(cconj(Q.ld(i * n + r, s)), C.ld(r, cs)));
         const cx<R> prev = pass == 0 ? zero : Rm.ld(i + rk, s);
         Rm.st(i + rk, s, cadd(prev, rik));
-#pragma unroll
-        for (int r = 0; r < NMAX; ++r)
-          if (r < n) ck[r] = csub(ck[r], cmul(rik, Q.ld(i * n + r, s)));
+PP_UNROLL_ROWS
+        for (int r = 0; r < n; ++r) C.st(r, cs, csub(C.ld(r, cs), cmul(rik, Q.ld(i * n + r, s))));
       }
     }
     R acc = rfrom<R>(0.0);
-#pragma unroll
-    for (int r = 0; r < NMAX; ++r)
-      if (r < n) acc = radd(acc, cabs2(ck[r]));
+PP_UNROLL_ROWS
+    for (int r = 0; r < n; ++r) acc = radd(acc, cabs2(C.ld(r, cs)));
     const R rkk = rsqrt(acc);
     if (rcmp(rkk, tol) <= 0) return false;
     Rm.st(k + rk, s, cx<R>{rkk, rfrom<R>(0.0)});
     const R rinv = rdiv(rfrom<R>(1.0), rkk);
     cx<R> y = zero;
-#pragma unroll
-    for (int r = 0; r < NMAX; ++r) {
-      if (r < n) {
-        ck[r] = cmulr(ck[r], rinv);
-        Q.st(k * n + r, s, ck[r]);
-        y = cadd(y, cmul(cconj(ck[r]), B.ld(r, s)));  // y_k = <q_k, b> (linalg.hpp:117)
-      }
+PP_UNROLL_ROWS
+    for (int r = 0; r < n; ++r) {
+      const cx<R> q = cmulr(C.ld(r, cs), rinv);
+      Q.st(k * n + r, s, q);
+      y = cadd(y, cmul(cconj(q), B.ld(r, s)));  // y_k = <q_k, b> (linalg.hpp:117)
     }
     Y.st(k, s, y);
   }
-  // back substitution R x = y (linalg.hpp:118-122)
-#pragma unroll
-  for (int j = NMAX - 1; j >= 0; --j) {
-    if (j < n) {
-      s = s_in;
-      asm volatile("" : "+l"(s));
-      Rm = Rm0.fresh();
-      Y = Y0.fresh();
-      cx<R> acc = Y.ld(j, s);
-#pragma unroll
-      for (int i = j + 1; i < NMAX; ++i)
-        if (i < n) acc = csub(acc, cmul(Rm.ld(j + i * (i + 1) / 2, s), dx[i]));
-      dx[j] = cdiv(acc, Rm.ld(j + j * (j + 1) / 2, s));
-    }
+  // back substitution R x = y (linalg.hpp:118-122); x_j overwrites C_j
+  for (int j = n - 1; j >= 0; --j) {
+    cx<R> acc = Y.ld(j, s);
+    for (int i = j + 1; i < n; ++i) acc = csub(acc, cmul(Rm.ld(j + i * (i + 1) / 2, s), C.ld(i, cs)));
+    C.st(j, cs, cdiv(acc, Rm.ld(j + j * (j + 1) / 2, s)));
   }
   return true;
 }
@@ -371,7 +364,7 @@ __global__ void __launch_bounds__(128, PP_EVAL_MINB) eval_trip(const TrackArgs a
   constexpr int L = level<R>::L;
   extern __shared__ double smem[];
   const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (s >= a.S) return;
+  if (s >= a.n_active) return;
   const SlotInts si{a.si, a.S};
   const int mode = si(F_MODE, s);
   if (mode != M_NEWTON && mode != M_REFINE && mode != M_FINAL) return;
@@ -392,32 +385,34 @@ __global__ void __launch_bounds__(128, PP_EVAL_MINB) eval_trip(const TrackArgs a
 // ---------------------------------------------------------------------------------------------
 // trip kernel 2: least-squares Newton update for corrector / refinement slots
 // ---------------------------------------------------------------------------------------------
-template <class R, int NMAX>
+template <class R>
 __global__ void __launch_bounds__(128, PP_LSQ_MINB) lsq_trip(const TrackArgs a) {
+  constexpr int L = level<R>::L;
+  extern __shared__ double smem[];
   const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (s >= a.S) return;
+  if (s >= a.n_active) return;
   const SlotInts si{a.si, a.S};
   const int mode = si(F_MODE, s);
   if (mode != M_NEWTON && mode != M_REFINE) return;
   const int n = a.plan.n;
   const Planar<R> X{a.x, a.S}, J{a.J, a.S}, Rm{a.Rm, a.S}, B{a.B, a.S}, Y{a.Y, a.S};
-  cx<R> dx[NMAX];
-  const bool ok = lsq_solve<R, NMAX>(n, a.rank_tol, J, Rm, B, Y, s, dx);
+  const Planar<R> C{smem, blockDim.x};
+  const size_t cs = threadIdx.x;
+  const bool ok = lsq_solve_c<R>(n, a.rank_tol, J, Rm, B, Y, s, C, cs);
   si(F_OK, s) = ok ? 1 : 0;
   if (!ok) return;
   // x += dx; update and iterate norms (tracker.cpp:258-264)
   double dxn = 0.0, xn = 0.0;
-#pragma unroll
-  for (int v = 0; v < NMAX; ++v) {
-    if (v < n) {
-      const cx<R> xv = cadd(X.ld(v, s), dx[v]);
-      X.st(v, s, xv);
-      dxn = f_max(dxn, cabsd(dx[v]));
-      xn = f_max(xn, cabsd(xv));
-    }
+  for (int v = 0; v < n; ++v) {
+    const cx<R> dv = C.ld(v, cs);
+    const cx<R> xv = cadd(X.ld(v, s), dv);
+    X.st(v, s, xv);
+    dxn = f_max(dxn, cabsd(dv));
+    xn = f_max(xn, cabsd(xv));
   }
   a.sd[D_DXN * a.S + s] = dxn;
   a.sd[D_XN * a.S + s] = xn;
+  (void)L;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -706,7 +701,7 @@ __device__ __forceinline__ int step_slot(const TrackArgs& a, size_t s, const Pla
 template <class R>
 __global__ void __launch_bounds__(128) step_trip(const TrackArgs a, unsigned* busy_out) {
   const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool in_range = s < a.S;
+  const bool in_range = s < a.n_active;
   int mode = M_DONE;
   if (in_range) {
     const SlotInts si{a.si, a.S};
@@ -727,70 +722,6 @@ __global__ void __launch_bounds__(128) step_trip(const TrackArgs a, unsigned* bu
     atomicAdd(a.work, static_cast<unsigned long long>(__popc(busy)));
     atomicAdd(a.work + 1, static_cast<unsigned long long>(__popc(solve)));
   }
-}
-
-// ---------------------------------------------------------------------------------------------
-// persistent kernel: one launch tracks every path of [lo, hi).  One thread owns one slot for the
-// whole launch and loops {control; heavy operation}; the heavy operation (evaluation, then the
-// least-squares update in corrector / refinement mode) is the same code for every lane of a
-// warp, so lanes run it converged although each is at its own place on its own path.  The
-// working point and the open Jacobian row live in shared memory; the slot state stays in the
-// SoA global arrays (touched once per iteration) so that only the heavy operation's working set
-// occupies registers.  A warp leaves the loop when all its lanes are done.
-// ---------------------------------------------------------------------------------------------
-template <class R, int NMAX, int KMAX>
-__global__ void __launch_bounds__(64) track_fused(const TrackArgs a) {
-  constexpr int L = level<R>::L;
-  extern __shared__ double smem[];
-  const size_t s0 = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // S = grid * block
-  const int n = a.plan.n;
-  const size_t ls0 = threadIdx.x;
-  const Planar<R> J{a.J, a.S}, Rm{a.Rm, a.S}, B{a.B, a.S}, Y{a.Y, a.S};
-
-  HeavyOut<R> ho;
-  ho.resid = ho.dxn = ho.xn = 0.0;
-  ho.resid_r = rfrom<R>(0.0);
-  ho.ok = false;
-  unsigned evals = 0, solves = 0;
-
-  for (;;) {
-    // launder the slot indices once per iteration: keeps the compiler from hoisting the many
-    // loop-invariant per-plane addresses out of the loop (they would pin registers for the
-    // whole launch and force spills in the heavy operation)
-    size_t s = s0, ls = ls0;
-    asm volatile("" : "+l"(s), "+l"(ls));
-    const Planar<R> X{smem, blockDim.x};
-    const Planar<R> JR{smem + static_cast<size_t>(n) * 2 * L * blockDim.x, blockDim.x};
-    const int mode = step_slot<R>(a, s, X, ls, ho);
-    if (__all_sync(0xffffffffu, mode == M_DONE)) break;
-    if (mode == M_NEWTON || mode == M_REFINE || mode == M_FINAL) {
-      const R te = mode == M_NEWTON ? (Planar<R>{a.sr, a.S}.ldr(R_TNEXT, s)) : rfrom<R>(1.0);
-      eval_hj<R, KMAX>(a.plan, X, JR, ls, te, B, J, s, ho.resid, ho.resid_r);
-      ++evals;
-    }
-    if (mode == M_NEWTON || mode == M_REFINE) {
-      cx<R> dx[NMAX];
-      ho.ok = lsq_solve<R, NMAX>(n, a.rank_tol, J, Rm, B, Y, s, dx);
-      ++solves;
-      if (ho.ok) {
-        // x += dx; update and iterate norms (tracker.cpp:258-264)
-        double dxn = 0.0, xn = 0.0;
-#pragma unroll
-        for (int v = 0; v < NMAX; ++v) {
-          if (v < n) {
-            const cx<R> xv = cadd(X.ld(v, ls), dx[v]);
-            X.st(v, ls, xv);
-            dxn = f_max(dxn, cabsd(dx[v]));
-            xn = f_max(xn, cabsd(xv));
-          }
-        }
-        ho.dxn = dxn;
-        ho.xn = xn;
-      }
-    }
-  }
-  atomicAdd(a.work, static_cast<unsigned long long>(evals));
-  atomicAdd(a.work + 1, static_cast<unsigned long long>(solves));
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -817,17 +748,16 @@ __global__ void __launch_bounds__(128) eval_kernel(const EvalArgs a) {
   for (int p = 0; p < a.plan.n_polys; ++p) B.st(p, s, cneg(B.ld(p, s)));
 }
 
-template <class R, int NMAX>
+template <class R>
 __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
+  extern __shared__ double smem[];
   const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s >= a.batch) return;
   const Planar<R> Q{a.a, a.batch}, Rm{a.r, a.batch}, B{a.b, a.batch}, Y{a.y, a.batch}, X{a.x, a.batch};
-  cx<R> dx[NMAX];
-  const bool ok = lsq_solve<R, NMAX>(a.n, a.rank_tol, Q, Rm, B, Y, s, dx);
+  const Planar<R> C{smem, blockDim.x};
+  const bool ok = lsq_solve_c<R>(a.n, a.rank_tol, Q, Rm, B, Y, s, C, threadIdx.x);
   a.ok[s] = ok ? 1 : 0;
-#pragma unroll
-  for (int v = 0; v < NMAX; ++v)
-    if (v < a.n) X.st(v, s, ok ? dx[v] : czero<R>());
+  for (int v = 0; v < a.n; ++v) X.st(v, s, ok ? C.ld(v, threadIdx.x) : czero<R>());
 }
 
 }  // namespace dev
@@ -836,8 +766,7 @@ __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
 // instantiate the three kernels of one (level, NMAX, KMAX) variant
 #define PP_VARIANT(R, NM, KM)                                                         \
   {NM, KM, reinterpret_cast<const void*>(&pp::dev::eval_trip<R, KM>),                 \
-   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, NM>),                          \
+   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R>),                          \
    reinterpret_cast<const void*>(&pp::dev::step_trip<R>),                             \
    reinterpret_cast<const void*>(&pp::dev::eval_kernel<R, KM>),                       \
-   reinterpret_cast<const void*>(&pp::dev::lsq_kernel<R, NM>),                       \
-   reinterpret_cast<const void*>(&pp::dev::track_fused<R, NM, KM>)}
+   reinterpret_cast<const void*>(&pp::dev::lsq_kernel<R>)}

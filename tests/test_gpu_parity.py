@@ -177,9 +177,14 @@ def test_cyclic10_dd_properties(pp, monkeypatch):
     b = pp.track_all(h, starts, lo=lo, hi=hi)
     monkeypatch.setenv("PP200_SLOTS_PER_SM", "128")
     monkeypatch.setenv("PP200_GRAPH_TRIPS", "3")
+    monkeypatch.setenv("PP200_COMPACT", "0")
     c = pp.track_all(h, starts, lo=lo, hi=hi)
     monkeypatch.delenv("PP200_SLOTS_PER_SM")
     monkeypatch.delenv("PP200_GRAPH_TRIPS")
+    monkeypatch.delenv("PP200_COMPACT")
+    monkeypatch.setenv("PP200_KERNEL_TIMING", "1")  # per-trip launches, compaction between trips
+    e = pp.track_all(h, starts, lo=lo, hi=hi)
+    monkeypatch.delenv("PP200_KERNEL_TIMING")
     mid = lo + 5000
     d1 = pp.track_all(h, starts, lo=lo, hi=mid)
     d2 = pp.track_all(h, starts, lo=mid, hi=hi)
@@ -187,6 +192,7 @@ def test_cyclic10_dd_properties(pp, monkeypatch):
         ref = getattr(a, k)
         assert np.array_equal(ref, getattr(b, k)), k
         assert np.array_equal(ref, getattr(c, k)), k
+        assert np.array_equal(ref, getattr(e, k)), k
         assert np.array_equal(ref, np.concatenate([getattr(d1, k), getattr(d2, k)])), k
 
 
