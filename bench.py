@@ -147,40 +147,38 @@ def profile_traffic(kernel: str):
 # ------------------------------------------------------------------------------------------------
 # CPU baseline / reference arm: the reference library (oracle/_ref) on the host cores
 # ------------------------------------------------------------------------------------------------
-def cpu_reference_sample(text: str, count: int, starts: list[tuple[int, int]], threads: int):
-    """track the given [lo, hi) ranges with the reference, one single-worker track_all per thread
-    (the reference's worker pool serialises concurrent callers; per-thread calls do not)"""
+def cpu_reference_sample(text: str, lo: int, hi: int, threads: int, budget_s: float):
+    """The reference tracker (oracle/_ref, the unmodified polypath build) on the host cores: each
+    thread tracks consecutive paths of its own group (groups spread over [lo, hi)) with
+    single-worker track_all calls until the time budget is spent.  (The reference's worker pool
+    serialises concurrent callers; independent single-worker calls per thread do not.)"""
     import oracle as O
 
     if O.ref is None:
         raise RuntimeError("oracle/_ref/libppref.so (the reference build) is not present")
-    kind = "reference"
     gam = complex(*_gamma_pair())
-    results = [None] * len(starts)
+    span = hi - lo
+    done = [0] * threads
+    t_end = time.perf_counter() + budget_s
 
-    def work(i, lo, hi):
-        results[i] = O.ref_track(text, PREC, gam, lo=lo, hi=hi, workers=1, batch=64)
-
-    pending = list(enumerate(starts))
-    lock = threading.Lock()
-
-    def worker():
-        while True:
-            with lock:
-                if not pending:
-                    return
-                i, (lo, hi) = pending.pop(0)
-            work(i, lo, hi)
+    def work(i):
+        p, limit, chunk = lo + span * i // threads, lo + span * (i + 1) // threads, 1
+        while p < limit and time.perf_counter() < t_end:
+            q = min(limit, p + chunk)
+            t0 = time.perf_counter()
+            O.ref_track(text, PREC, gam, lo=p, hi=q, workers=1, batch=64)
+            done[i] += q - p
+            if time.perf_counter() - t0 < 0.05:
+                chunk = min(chunk * 2, 64)
+            p = q
 
     t0 = time.perf_counter()
-    ths = [threading.Thread(target=worker) for _ in range(threads)]
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
     for t in ths:
         t.start()
     for t in ths:
         t.join()
-    wall = time.perf_counter() - t0
-    paths = sum(hi - lo for lo, hi in starts)
-    return paths, wall, kind
+    return sum(done), time.perf_counter() - t0, "reference"
 
 
 def _gamma_pair():
@@ -190,13 +188,6 @@ def _gamma_pair():
     return g.real, g.imag
 
 
-def sample_ranges(count: int, B: int, c: int, threads: int, per_thread: int):
-    """per_thread consecutive paths for each thread, spread across chunk c"""
-    off = chunk_offset(c, count, B)
-    stride = max(per_thread, B // threads)
-    return [(off + i * stride, off + i * stride + per_thread) for i in range(threads)]
-
-
 def run_reference_arm(args, world, rank):
     if rank != 0:
         return
@@ -204,25 +195,24 @@ def run_reference_arm(args, world, rank):
         text = fh.read()
     count = 3628800
     threads = os.cpu_count() or 1
-    per_thread = args.cpu_paths_per_thread
     total_paths, total_wall, kind = 0, 0.0, "reference"
     for s in range(args.warmup + args.steps):
-        rngs = sample_ranges(count, args.paths, s, threads, per_thread)
-        paths, wall, kind = cpu_reference_sample(text, count, rngs, threads)
+        lo = chunk_offset(s, count, args.paths)
+        paths, wall, kind = cpu_reference_sample(text, lo, lo + args.paths, threads, args.cpu_budget)
         if s >= args.warmup:
             total_paths += paths
             total_wall += wall
     value = total_paths / total_wall
+    sample = (f"each step: {args.cpu_budget:.0f} s of single-worker reference track_all calls on {threads} threads over "
+              f"the step's chunk of {args.paths} start paths; {total_paths} paths timed over {args.steps} steps")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "paths/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_wall / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "dd (binary64 pairs)",
         "data": "synthetic: total-degree start solutions of cyclic-10, gamma = random_gamma(1)",
         "config": {"workload": "cyclic10 total-degree homotopy, complex double-double, TrackConfig::defaults(dd)",
-                   "sample": f"{threads} threads x {per_thread} paths per step (bounded sample of each step's chunk)",
-                   "cpu_threads": threads},
-        "cpu_baseline": {"value": value, "unit": "paths/s", "cores": threads, "kind": kind,
-                         "sample": f"{args.steps} steps x {threads * per_thread} paths, single-worker track_all per thread"},
+                   "paths_per_step_per_gpu": args.paths, "cpu_threads": threads},
+        "cpu_baseline": {"value": value, "unit": "paths/s", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "paths/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -291,12 +281,18 @@ def run_ours(args, world, rank, local, dist):
     if rank != 0:
         return
 
-    # roofline of the dominant kernel: one instrumented step (per-kernel CUDA events)
+    # roofline of the dominant kernel: one instrumented step (every trip's kernels bracketed by CUDA
+    # events on the library's stream; per-trip log for the steady-state rates)
+    import tempfile
+
+    log = tempfile.NamedTemporaryFile(prefix="pp200_trips_", suffix=".txt", delete=False).name
     os.environ["PP200_KERNEL_TIMING"] = "1"
+    os.environ["PP200_TRIP_LOG"] = log
     try:
         sol_i, _ = step(args.warmup + args.steps)
     finally:
         os.environ.pop("PP200_KERNEL_TIMING", None)
+        os.environ.pop("PP200_TRIP_LOG", None)
     sti = sol_i.stats
     work = W.path_work(info, PREC, sti["evals"], sti["solves"])
     lsq_rate = work["lsq_total"] / (sti["lsq_ms"] / 1e3)
@@ -306,14 +302,30 @@ def run_ours(args, world, rank, local, dist):
     peak_ops = fp64_peak_ops(local)
     peak = peak_ops / 1e12 if peak_ops else None
     shares = {k: sti[k] / max(1e-9, sti["eval_ms"] + sti["lsq_ms"] + sti["step_ms"]) for k in ("eval_ms", "lsq_ms", "step_ms")}
+    steady = None
+    try:
+        t = np.loadtxt(log, ndmin=2)
+        full = t[:, 1] >= t[:, 5]  # trips on which every launched slot was busy
+        if full.any() and peak_ops:
+            steady = {"trips": int(full.sum()), "of_trips": len(t),
+                      "eval_frac": float((t[full, 1] * work["eval_ops"]).sum() / (t[full, 2].sum() / 1e3) / peak_ops),
+                      "lsq_frac": float((t[full, 1] * work["lsq_ops"]).sum() / (t[full, 3].sum() / 1e3) / peak_ops),
+                      "busy_weighted_slot_use": float(t[:, 1].sum() / t[:, 5].sum())}
+        os.unlink(log)
+    except Exception:  # noqa: BLE001
+        pass
     roofline = {
         "bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
         "frac": (achieved / peak) if peak else None,
         "traffic": profile_traffic(dominant),
         "kernel": dominant,
-        "op_convention": "binary64 pipe ops (DADD/DMUL/DFMA = 1 each) of the reference arithmetic per Newton iteration",
-        "peak_source": "measured FP64 pipe rate (pp_fp64_peak microbenchmark, this GPU)",
+        "op_convention": "binary64 pipe ops (DADD/DMUL/DFMA = 1 each) of the reference arithmetic",
+        "peak_source": "measured FP64 pipe rate (pp_fp64_peak: independent DFMA chains, this GPU); "
+                       "MEASURED_PEAKS.json has no FP64 figure",
+        "achieved_def": "algorithmic ops of all launches of the kernel in one instrumented step / their summed "
+                        "CUDA-event time (tail trips with few busy slots included)",
         "eval_trip_tflops": eval_rate / 1e12, "lsq_trip_tflops": lsq_rate / 1e12,
+        "steady_state": steady,
         "kernel_time_share": shares,
         "ops_per_unit": {"eval": work["eval_ops"], "lsq": work["lsq_ops"]},
         "units": {"evals": sti["evals"], "solves": sti["solves"]},
@@ -324,12 +336,12 @@ def run_ours(args, world, rank, local, dist):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        rngs = sample_ranges(count, B, args.warmup, threads, args.cpu_paths_per_thread)
+        lo = chunk_offset(args.warmup, count, B)
         try:
-            cp, cw, kind = cpu_reference_sample(text, count, rngs, threads)
+            cp, cw, kind = cpu_reference_sample(text, lo, lo + B, threads, args.cpu_budget)
             cpu = {"value": cp / cw, "unit": "paths/s", "cores": threads, "kind": kind,
-                   "sample": f"{cp} paths ({threads} threads x {args.cpu_paths_per_thread} consecutive paths "
-                             f"spread over step {args.warmup}'s chunk), single-worker reference track_all per thread"}
+                   "sample": f"{cp} paths of step {args.warmup}'s chunk in {cw:.1f} s: {threads} threads, each "
+                             f"single-worker reference track_all calls over its own slice of the chunk"}
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": "paths/s", "cores": threads, "kind": "reference",
                    "sample": f"unavailable: {exc}"}
@@ -361,8 +373,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--paths", type=int, default=65536, help="start paths per step per GPU")
-    ap.add_argument("--cpu-paths-per-thread", type=int, default=4)
+    ap.add_argument("--paths", type=int, default=262144, help="start paths per step per GPU")
+    ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of reference CPU tracking per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     world, rank, local, dist = dist_setup()

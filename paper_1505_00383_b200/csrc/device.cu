@@ -279,8 +279,12 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   const size_t per_thread_smem = static_cast<size_t>(2) * n * 2 * L * sizeof(double);
   int tblock = static_cast<int>(std::min<size_t>(128, std::max<size_t>(32, env_size("PP200_TRIP_BLOCK", kBlock))));
   while (tblock > 32 && static_cast<size_t>(tblock) * per_thread_smem > 200 * 1024) tblock /= 2;
-  const size_t eval_smem = static_cast<size_t>(tblock) * per_thread_smem;
-  const size_t lsq_smem = eval_smem / 2;  // the column being orthogonalised
+  // the evaluation kernel may run narrower blocks than the others (its shared memory -- point
+  // and open Jacobian row per thread -- is what limits its occupancy)
+  int eblock = static_cast<int>(std::min<size_t>(tblock, std::max<size_t>(32, env_size("PP200_EVAL_BLOCK", tblock))));
+  while (tblock % eblock != 0) eblock /= 2;
+  const size_t eval_smem = static_cast<size_t>(eblock) * per_thread_smem;
+  const size_t lsq_smem = static_cast<size_t>(tblock) * per_thread_smem / 2;  // the column being orthogonalised
   check(cudaFuncSetAttribute(var->eval_trip, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(eval_smem)),
         "cudaFuncSetAttribute");
   check(cudaFuncSetAttribute(var->lsq_trip, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsq_smem)),
@@ -405,6 +409,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   {
     const dim3 blk(tblock);
     dim3 grid(static_cast<unsigned>(blocks));
+    auto egrid = [&]() { return dim3(grid.x * static_cast<unsigned>(tblock / eblock)); };
     void* targs[] = {&a};
     unsigned* busy_slot = busy;
     void* sargs[] = {&a, &busy_slot};
@@ -456,7 +461,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
         check(cudaMemsetAsync(busy, 0, sizeof(unsigned), stream), "memset busy");
         void* sa[] = {&a, &busy_slot};
         cudaEventRecord(ev[0], stream);
-        check(cudaLaunchKernel(var->eval_trip, grid, blk, targs, eval_smem, stream), "launch eval_trip");
+        check(cudaLaunchKernel(var->eval_trip, egrid(), dim3(eblock), targs, eval_smem, stream), "launch eval_trip");
         cudaEventRecord(ev[1], stream);
         check(cudaLaunchKernel(var->lsq_trip, grid, blk, targs, lsq_smem, stream), "launch lsq_trip");
         cudaEventRecord(ev[2], stream);
@@ -497,7 +502,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
         for (size_t j = 0; j < graph_trips; ++j) {
           busy_ptrs[j] = busy + j;
           void* sa[] = {&a, &busy_ptrs[j]};
-          check(cudaLaunchKernel(var->eval_trip, grid, blk, targs, eval_smem, stream), "launch eval_trip");
+          check(cudaLaunchKernel(var->eval_trip, egrid(), dim3(eblock), targs, eval_smem, stream), "launch eval_trip");
           check(cudaLaunchKernel(var->lsq_trip, grid, blk, targs, lsq_smem, stream), "launch lsq_trip");
           check(cudaLaunchKernel(var->step_trip, grid, blk, sa, 0, stream), "launch step_trip");
         }

@@ -34,6 +34,9 @@
 #ifndef PP_EVAL_MINB
 #define PP_EVAL_MINB 1
 #endif
+#ifndef PP_EVAL_ROLLED
+#define PP_EVAL_ROLLED 1
+#endif
 
 namespace pp {
 namespace dev {
@@ -226,6 +229,30 @@ __device__ void eval_hj(const PlanArgs& pa, const Planar<R>& X, const Planar<R>&
 
     // Speelpenning products (evaldiff.cpp:90-115): prefix P_j = x_p0 ... x_p(j-1) for j < k,
     // value = P_(k-1) x_p(k-1), d_j = P_j * S_(j+1) with the running suffix S.
+#if PP_EVAL_ROLLED
+    // rolled: the prefix stack is a dynamically indexed (local-memory, L1-resident) array, so
+    // the term loop is compact code whatever KMAX is
+    cx<R> P[KMAX > 1 ? KMAX : 2];
+    cx<R> run = X.ld(static_cast<int>(__ldg(pv) & 0xffffu), ls);
+    P[1] = run;
+    for (int j = 2; j < k; ++j) {
+      run = cmul(run, X.ld(static_cast<int>(__ldg(pv + j - 1) & 0xffffu), ls));
+      P[j] = run;
+    }
+    const uint32_t plast = __ldg(pv + k - 1);
+    const cx<R> xlast = X.ld(static_cast<int>(plast & 0xffffu), ls);
+    cx<R> val = cmul(run, xlast);
+    if (nb > 0) val = cmul(val, aux);
+    sacc = cadd(sacc, cmul(c, val));
+    contribute(plast, run);  // d_(k-1) = P_(k-1)
+    cx<R> acc = xlast;
+    for (int j = k - 2; j >= 1; --j) {
+      const uint32_t pj = __ldg(pv + j);
+      const cx<R> d = cmul(P[j], acc);
+      acc = cmul(acc, X.ld(static_cast<int>(pj & 0xffffu), ls));
+      contribute(pj, d);
+    }
+#else
     cx<R> P[KMAX > 1 ? KMAX : 2];
     cx<R> run = X.ld(static_cast<int>(__ldg(pv) & 0xffffu), ls);
     P[1] = run;
@@ -252,6 +279,7 @@ __device__ void eval_hj(const PlanArgs& pa, const Planar<R>& X, const Planar<R>&
         contribute(pj, d);
       }
     }
+#endif
     contribute(__ldg(pv), acc);  // d_0 = S_1
   }
   while (cur < np) flush(cur++);
@@ -272,13 +300,34 @@ __device__ void eval_hj(const PlanArgs& pa, const Planar<R>& X, const Planar<R>&
 #define PP_STR(x) PP_STR_(x)
 #define PP_UNROLL_ROWS _Pragma(PP_STR(unroll PP_LSQ_UNROLL))
 
-__device__ __forceinline__ void prefetch_l1(const double* p) { asm volatile("prefetch.L1 [%0];" ::"l"(p)); }
+// PP_LSQ_PREFETCH: 0 none, 1 into L1, 2 into L2 (the next column to be read)
+#ifndef PP_LSQ_PREFETCH
+#define PP_LSQ_PREFETCH 1
+#endif
+// PP_LSQ_PIPE: software-pipelined row loops (row r+1 of q loaded while row r is computed)
+#ifndef PP_LSQ_PIPE
+#define PP_LSQ_PIPE 0
+#endif
+
+__device__ __forceinline__ void prefetch_line(const double* p) {
+#if PP_LSQ_PREFETCH == 1
+  asm volatile("prefetch.L1 [%0];" ::"l"(p));
+#elif PP_LSQ_PREFETCH == 2
+  asm volatile("prefetch.L2 [%0];" ::"l"(p));
+#else
+  (void)p;
+#endif
+}
 
 template <class R>
 __device__ __forceinline__ void prefetch_column(const Planar<R>& Q, int col, int n, size_t s) {
+#if PP_LSQ_PREFETCH
   constexpr int L = level<R>::L;
   const double* p = Q.base + static_cast<size_t>(col) * n * 2 * L * Q.S + s;
-  for (int e = 0; e < n * 2 * L; ++e) prefetch_l1(p + static_cast<size_t>(e) * Q.S);
+  for (int e = 0; e < n * 2 * L; ++e) prefetch_line(p + static_cast<size_t>(e) * Q.S);
+#else
+  (void)Q, (void)col, (void)n, (void)s;
+#endif
 }
 
 template <class R>
@@ -306,12 +355,29 @@ PP_UNROLL_ROWS
         const int nxt = i + 1 < k ? i + 1 : (pass == 0 ? 0 : k + 1);
         if (nxt < n) prefetch_column<R>(Q, nxt, n, s);
         cx<R> rik = zero;
+#if PP_LSQ_PIPE
+        cx<R> qn = Q.ld(i * n, s);
+        for (int r = 0; r < n; ++r) {
+          const cx<R> q = qn;
+          if (r + 1 < n) qn = Q.ld(i * n + r + 1, s);
+          rik = cadd(rik, cmul(cconj(q), C.ld(r, cs)));
+        }
+        const cx<R> prev = pass == 0 ? zero : Rm.ld(i + rk, s);
+        Rm.st(i + rk, s, cadd(prev, rik));
+        qn = Q.ld(i * n, s);
+        for (int r = 0; r < n; ++r) {
+          const cx<R> q = qn;
+          if (r + 1 < n) qn = Q.ld(i * n + r + 1, s);
+          C.st(r, cs, csub(C.ld(r, cs), cmul(rik, q)));
+        }
+#else
 PP_UNROLL_ROWS
         for (int r = 0; r < n; ++r) rik = cadd(rik, cmul(cconj(Q.ld(i * n + r, s)), C.ld(r, cs)));
         const cx<R> prev = pass == 0 ? zero : Rm.ld(i + rk, s);
         Rm.st(i + rk, s, cadd(prev, rik));
 PP_UNROLL_ROWS
         for (int r = 0; r < n; ++r) C.st(r, cs, csub(C.ld(r, cs), cmul(rik, Q.ld(i * n + r, s))));
+#endif
       }
     }
     R acc = rfrom<R>(0.0);
