@@ -193,6 +193,18 @@ int pp_eval_batch(const pp_homotopy* h, uint32_t batch, const double* points, co
 int pp_lsq_batch(int prec, uint32_t n, uint32_t batch, const double* a, const double* b,
                  double* x, uint8_t* ok, int device);
 
+/*
+ * Output records as the reference CLI writes them (polypath_main.cpp:125-189):
+ * one JSON "solution" line per record (coordinates as full-precision decimal strings, to_decimal
+ * of xprec_io.cpp:31-108), then one "summary" line.  gamma is 2L doubles.  Two-call pattern:
+ * returns PP_E_CAPACITY with *needed = bytes required (including the NUL) when buf is too small.
+ */
+int pp_solutions_jsonl(const pp_records* rec, int prec, uint32_t dim, const double* gamma, uint64_t seed,
+                       const char* command, double wall_ms, uint64_t batches, uint64_t rounds, char* buf,
+                       size_t cap, size_t* needed);
+/* to_decimal of one level value (xprec_io.cpp:31-108, 198-212): 17 / 32 / 64 significant digits */
+int pp_to_decimal(int prec, const double* limbs, char* buf, size_t cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -158,6 +158,9 @@ _sig("pp_homotopy_free", None, _vp)
 _sig("pp_track_config_defaults", None, _i32, _P(TrackConfigC))
 _sig("pp_track_config_validate", _i32, _P(TrackConfigC))
 _sig("pp_track_all", _i32, _vp, _vp, _P(TrackConfigC), _u64, _u64, _i32, _P(RecordsC), _P(RunStatsC))
+_sig("pp_solutions_jsonl", _i32, _vp, _i32, _u32, _vp, _u64, ctypes.c_char_p, _dbl, _u64, _u64, ctypes.c_char_p,
+     _sz, _P(_sz))
+_sig("pp_to_decimal", _i32, _i32, _vp, ctypes.c_char_p, _sz)
 _sig("pp_eval_batch", _i32, _vp, _u32, _vp, _vp, _vp, _vp, _i32)
 _sig("pp_lsq_batch", _i32, _i32, _u32, _u32, _vp, _vp, _vp, _vp, _i32)
 _sig("pp_test_arith", _i32, _i32, _i32, _vp, _vp, _vp)
@@ -171,7 +174,8 @@ EXPORTED = [
     "pp_system_stats", "pp_system_degrees", "pp_system_free", "pp_random_gamma", "pp_total_degree_start",
     "pp_load_start_data", "pp_starts_explicit", "pp_starts_roots", "pp_starts_count", "pp_starts_solution", "pp_starts_free",
     "pp_make_homotopy", "pp_homotopy_info", "pp_homotopy_free", "pp_track_config_defaults",
-    "pp_track_config_validate", "pp_track_all", "pp_eval_batch", "pp_lsq_batch",
+    "pp_track_config_validate", "pp_track_all", "pp_eval_batch", "pp_lsq_batch", "pp_solutions_jsonl",
+    "pp_to_decimal",
 ]
 
 
@@ -444,6 +448,28 @@ class SolutionSet:
         return (((re[..., 3] + re[..., 2]) + re[..., 1]) + re[..., 0]) + 1j * (
             ((im[..., 3] + im[..., 2]) + im[..., 1]) + im[..., 0])
 
+    def to_jsonl(self, gamma, seed: int = 1, command: str = "solve", wall_ms: float | None = None) -> str:
+        """The reference CLI's output (polypath_main.cpp:125-189): one JSON "solution" line per
+        record with full-precision decimal coordinates, then the "summary" line.  gamma is the
+        homotopy's gamma (complex, or 2L limbs)."""
+        L = LIMBS[self.prec]
+        g = np.ascontiguousarray(gamma_limbs(gamma, self.prec) if np.isscalar(gamma) else gamma, dtype=np.float64)
+        arrs = [np.ascontiguousarray(a) for a in (self.path_id, self.status, self.reason, self.steps,
+                                                   self.newton_iters, self.rejections, self.x, self.residual)]
+        rec = RecordsC(len(self), len(self), *[_ptr(a) for a in arrs])
+        dim = self.x.shape[1] if self.x.ndim == 3 else 0
+        wall = self.stats.get("wall_ms", 0.0) if wall_ms is None else wall_ms
+        args = (ctypes.byref(rec), _prec(self.prec), dim, _ptr(g), seed, command.encode(), float(wall),
+                int(self.stats.get("batches", 1)), int(self.stats.get("total_rounds", 0)))
+        need = _sz()
+        rc = lib.pp_solutions_jsonl(*args, None, 0, ctypes.byref(need))
+        if rc not in (0, -5):
+            _check(rc)
+        buf = ctypes.create_string_buffer(need.value)
+        _check(lib.pp_solutions_jsonl(*args, buf, need.value, ctypes.byref(need)))
+        del L
+        return buf.value.decode()
+
     def counts(self):
         out = {"converged": int(np.sum(self.status == SUCCESS))}
         for r, name in enumerate(REASONS[1:], start=1):
@@ -532,18 +558,19 @@ def host_arith(prec, op: int, a, b) -> np.ndarray:
     return out
 
 
+def to_decimal(prec, limbs) -> str:
+    """to_decimal at a level (xprec_io.cpp:31-108): 17 / 32 / 64 significant digits."""
+    a = np.zeros(4)
+    a[: len(limbs)] = limbs
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.pp_to_decimal(_prec(prec), _ptr(a), buf, 128))
+    return buf.value.decode()
+
+
 def parse_decimal(prec, s: str) -> np.ndarray:
     out = np.zeros(4)
     _check(lib.pp_test_parse_decimal(_prec(prec), s.encode(), _ptr(out)))
     return out[: LIMBS[_pname(prec)]]
-
-
-def to_decimal(prec, limbs) -> str:
-    a = np.zeros(4)
-    a[: len(limbs)] = limbs
-    buf = ctypes.create_string_buffer(128)
-    _check(lib.pp_test_to_decimal(_prec(prec), _ptr(a), buf, 128))
-    return buf.value.decode()
 
 
 __all__ = [

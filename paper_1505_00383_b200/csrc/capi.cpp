@@ -5,8 +5,11 @@
 // reference throws: InvalidArgument -> PP_E_INVALID (std::invalid_argument), ParseFailure ->
 // PP_E_PARSE (polypath::ParseError), CudaFailure -> PP_E_CUDA.
 
+#include <algorithm>
+#include <charconv>
 #include <cstring>
 #include <map>
+#include <vector>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -427,6 +430,132 @@ int pp_lsq_batch(int prec, uint32_t n, uint32_t batch, const double* a, const do
     need(limbs_of(prec) > 0 && n >= 1, "pp_lsq_batch: bad argument");
     need(batch == 0 || (a && b && x && ok), "pp_lsq_batch: null argument");
     pp::device_lsq(prec, n, batch, a, b, x, ok, device);
+    return PP_OK;
+  });
+}
+
+// ---- output records: the reference CLI's JSON lines (polypath_main.cpp:125-189) ----
+}  // extern "C"
+
+namespace {
+// a double as nlohmann::json::dump prints it: shortest round-trip digits, ".0" on integral values
+void put_double(std::string& o, double v) {
+  char b[64];
+  auto r = std::to_chars(b, b + sizeof b, v);
+  std::string t(b, r.ptr);
+  if (t.find_first_of(".eEn") == std::string::npos) t += ".0";
+  o += t;
+}
+std::string limbs_decimal(int prec, const double* p) {
+  return prec == PP_D ? pp::to_decimal_d(p[0])
+         : prec == PP_DD ? pp::to_decimal_dd(pp::dd_t{p[0], p[1]})
+                         : pp::to_decimal_qd(pp::qd_t{p[0], p[1], p[2], p[3]});
+}
+// to_double of a level value (xprec.hpp: DD hi + lo; QD ((c3 + c2) + c1) + c0)
+double limbs_to_double(int prec, const double* p) {
+  return prec == PP_D ? p[0] : prec == PP_DD ? pp::rtod(pp::dd_t{p[0], p[1]}) : pp::rtod(pp::qd_t{p[0], p[1], p[2], p[3]});
+}
+const char* reason_name(int r) {  // fail_reason_name (tracker.cpp:10-19)
+  switch (r) {
+    case PP_REASON_NONE: return "converged";
+    case PP_REASON_DIVERGED: return "diverged";
+    case PP_REASON_STEP_UNDERFLOW: return "step-underflow";
+    case PP_REASON_MAX_STEPS: return "max-steps";
+    case PP_REASON_SINGULAR: return "singular";
+    default: return "no-certificate";
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int pp_solutions_jsonl(const pp_records* rec, int prec, uint32_t dim, const double* gamma, uint64_t seed,
+                       const char* command, double wall_ms, uint64_t batches, uint64_t rounds, char* buf,
+                       size_t cap, size_t* needed) {
+  return guard([&] {
+    const int L = limbs_of(prec);
+    need(rec != nullptr && L > 0 && gamma != nullptr && needed != nullptr, "pp_solutions_jsonl: bad argument");
+    std::string o;
+    uint64_t converged = 0, diverged = 0, failed = 0;
+    std::vector<double> resid;
+    for (uint64_t i = 0; i < rec->count; ++i) {
+      const double res = limbs_to_double(prec, rec->residual + i * L);
+      const char* cls = rec->status[i] == PP_SUCCESS ? "converged"
+                        : rec->reason[i] == PP_REASON_DIVERGED ? "diverged" : "failed";
+      if (rec->status[i] == PP_SUCCESS) {
+        ++converged;
+        resid.push_back(res);
+      } else if (rec->reason[i] == PP_REASON_DIVERGED) {
+        ++diverged;
+      } else {
+        ++failed;
+      }
+      // record_json (polypath_main.cpp:133-150); keys in nlohmann's (sorted) order
+      o += "{\"annotation\":\"";
+      o += reason_name(rec->reason[i]);
+      o += "\",\"newton\":" + std::to_string(rec->newton_iters[i]);
+      o += ",\"path\":" + std::to_string(rec->path_id[i]);
+      o += ",\"rejections\":" + std::to_string(rec->rejections[i]);
+      o += ",\"residual\":";
+      put_double(o, res);
+      o += ",\"start\":" + std::to_string(rec->path_id[i]);
+      o += ",\"status\":\"";
+      o += cls;
+      o += "\",\"steps\":" + std::to_string(rec->steps[i]);
+      o += ",\"type\":\"solution\",\"wall_ms\":";
+      put_double(o, wall_ms);
+      o += ",\"x\":[";
+      for (uint32_t v = 0; v < dim; ++v) {
+        const double* z = rec->x + (i * dim + v) * 2 * L;
+        o += v ? ",[\"" : "[\"";
+        o += limbs_decimal(prec, z);
+        o += "\",\"";
+        o += limbs_decimal(prec, z + L);
+        o += "\"]";
+      }
+      o += "]}\n";
+    }
+    // summary (polypath_main.cpp:170-188)
+    std::sort(resid.begin(), resid.end());
+    o += "{\"batches\":" + std::to_string(batches);
+    o += ",\"command\":\"" + std::string(command ? command : "solve") + "\"";
+    o += ",\"converged\":" + std::to_string(converged);
+    o += ",\"corrector_rounds\":" + std::to_string(rounds);
+    o += ",\"diverged\":" + std::to_string(diverged);
+    o += ",\"failed\":" + std::to_string(failed);
+    o += ",\"gamma\":[";
+    put_double(o, limbs_to_double(prec, gamma));
+    o += ",";
+    put_double(o, limbs_to_double(prec, gamma + L));
+    o += "],\"paths\":" + std::to_string(rec->count);
+    o += ",\"precision\":\"";
+    o += prec == PP_D ? "d" : prec == PP_DD ? "dd" : "qd";
+    o += "\"";
+    if (!resid.empty()) {
+      o += ",\"residual_max\":";
+      put_double(o, resid.back());
+      o += ",\"residual_median\":";
+      put_double(o, resid[resid.size() / 2]);
+      o += ",\"residual_min\":";
+      put_double(o, resid.front());
+    }
+    o += ",\"seed\":" + std::to_string(seed);
+    o += ",\"type\":\"summary\",\"wall_ms\":";
+    put_double(o, wall_ms);
+    o += "}\n";
+    *needed = o.size() + 1;
+    if (buf == nullptr || cap < o.size() + 1) return PP_E_CAPACITY;
+    std::memcpy(buf, o.c_str(), o.size() + 1);
+    return PP_OK;
+  });
+}
+
+int pp_to_decimal(int prec, const double* limbs, char* buf, size_t cap) {
+  return guard([&] {
+    need(limbs_of(prec) > 0 && limbs != nullptr, "pp_to_decimal: bad argument");
+    const std::string t = limbs_decimal(prec, limbs);
+    if (buf == nullptr || cap < t.size() + 1) return PP_E_CAPACITY;
+    std::memcpy(buf, t.c_str(), t.size() + 1);
     return PP_OK;
   });
 }

@@ -4,7 +4,7 @@ gamma, TrackConfig -- each checked bit for bit against the reference build or it
 import numpy as np
 import pytest
 
-from conftest import read
+from conftest import golden, read
 
 
 def need_ref(O):
@@ -162,3 +162,36 @@ def test_track_config_defaults_and_validation(pp, oracle_mod):
             setattr(c, k, v)
         with pytest.raises(pp.InvalidArgument):
             c.validate()
+
+
+def test_solutions_jsonl_matches_the_reference_cli_format(pp, oracle_mod):
+    """pp_solutions_jsonl writes the reference CLI's records (polypath_main.cpp:125-189): decimal
+    coordinates that parse back bit for bit, to_decimal equal to the reference's, counts/summary"""
+    import json
+
+    g = golden("track_cyclic5_dd")
+    n = len(g["status"])
+    sol = pp.SolutionSet("dd", np.arange(n, dtype=np.uint64), g["status"], g["reason"], g["steps"],
+                         g["newton_iters"], g["rejections"], g["x"], g["residual"], {"wall_ms": 12.5, "total_rounds": 7})
+    lines = [json.loads(ln) for ln in sol.to_jsonl(pp.random_gamma(1), seed=1).splitlines()]
+    recs, summ = lines[:-1], lines[-1]
+    assert len(recs) == n and summ["type"] == "summary" and summ["paths"] == n
+    assert summ["converged"] == 70 and summ["diverged"] == 50 and summ["failed"] == 0
+    assert summ["precision"] == "dd" and summ["corrector_rounds"] == 7
+    assert sorted(recs[0].keys()) == list(recs[0].keys())  # nlohmann's sorted key order
+    for i, r in enumerate(recs):
+        assert r["path"] == r["start"] == i and r["type"] == "solution"
+        assert r["status"] == ("converged" if g["status"][i] == 1 else "diverged" if g["reason"][i] == 1 else "failed")
+        assert r["annotation"] == pp.REASONS[g["reason"][i]]
+        assert r["steps"] == g["steps"][i] and r["newton"] == g["newton_iters"][i]
+        assert r["residual"] == float(g["residual"][i][0] + g["residual"][i][1])
+        for v, (re, im) in enumerate(r["x"]):
+            # 32 significant digits: the parsed value is within a couple of dd ulps of the limbs
+            for txt, limbs in ((re, g["x"][i, v, :2]), (im, g["x"][i, v, 2:])):
+                back = pp.parse_decimal("dd", txt)
+                assert abs((back[0] - limbs[0]) + (back[1] - limbs[1])) <= 1e-30 * max(1.0, abs(limbs[0]))
+    if oracle_mod.ref is not None:
+        for i in (0, 3, 77):
+            for v in range(5):
+                assert recs[i]["x"][v][0] == oracle_mod.ref_to_decimal("dd", g["x"][i, v, :2])
+                assert recs[i]["x"][v][1] == oracle_mod.ref_to_decimal("dd", g["x"][i, v, 2:])
