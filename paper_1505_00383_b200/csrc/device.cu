@@ -114,6 +114,9 @@ struct DevicePlan {
   uint32_t* pos = nullptr;
   uint32_t* base = nullptr;
   double* coeff = nullptr;
+  uint32_t* term_slot = nullptr;
+  uint32_t* acc_off = nullptr;
+  uint32_t* acc_idx = nullptr;
 };
 
 namespace {
@@ -123,6 +126,10 @@ dev::PlanArgs plan_args(const Plan& plan, const DevicePlan* dp) {
   pa.pos = dp->pos;
   pa.base = dp->base;
   pa.coeff = dp->coeff;
+  pa.term_slot = dp->term_slot;
+  pa.acc_off = dp->acc_off;
+  pa.acc_idx = dp->acc_idx;
+  pa.n_slots = static_cast<int>(plan.n_slots());
   pa.n = static_cast<int>(plan.dim);
   pa.n_polys = static_cast<int>(plan.n_polys);
   pa.n_terms = static_cast<int>(plan.n_terms());
@@ -235,6 +242,9 @@ DevicePlan* device_plan_upload(const Plan& plan, int device) {
     dp->pos = upload(plan.pos);
     dp->base = upload(plan.base);
     dp->coeff = upload(plan.coeff);
+    dp->term_slot = upload(plan.term_slot);
+    dp->acc_off = upload(plan.acc_off);
+    dp->acc_idx = upload(plan.acc_idx);
   } catch (...) {
     device_plan_free(dp);
     throw;
@@ -251,6 +261,9 @@ void device_plan_free(DevicePlan* dp) {
   cudaFree(dp->pos);
   cudaFree(dp->base);
   cudaFree(dp->coeff);
+  cudaFree(dp->term_slot);
+  cudaFree(dp->acc_off);
+  cudaFree(dp->acc_idx);
   if (prev >= 0) cudaSetDevice(prev);
   delete dp;
 }
@@ -410,7 +423,41 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     const dim3 blk(tblock);
     dim3 grid(static_cast<unsigned>(blocks));
     auto egrid = [&]() { return dim3(grid.x * static_cast<unsigned>(tblock / eblock)); };
+    cudaEvent_t* timing_ev = nullptr;  // set while per-kernel events are recorded
     void* targs[] = {&a};
+
+    // tail mode (PP200_TAIL_SLOTS, default 8 per SM; 0 disables): once compaction has shrunk the
+    // launch to at most that many slots, each remaining path gets a whole warp (eval_coop /
+    // lsq_coop), bitwise identical to the thread-per-path kernels
+    const size_t el = static_cast<size_t>(2) * L * sizeof(double);  // bytes per complex value
+    const size_t ecoop_warp = (static_cast<size_t>(n) + plan.n_slots()) * el;
+    const size_t lcoop_warp = (static_cast<size_t>(n) * n + 4 * n + n * (n + 1) / 2) * el;
+    const int ewpb = static_cast<int>(std::min<size_t>(4, (200 * 1024) / ecoop_warp));
+    const int lwpb = static_cast<int>(std::min<size_t>(4, (200 * 1024) / lcoop_warp));
+    const size_t tail_slots = env_size("PP200_TAIL_SLOTS", 8 * static_cast<size_t>(prop.multiProcessorCount));
+    // PP200_FORCE_COOP=1 runs every trip in tail mode (used by the parity tests)
+    bool coop = env_size("PP200_FORCE_COOP", 0) != 0 && ewpb >= 1 && lwpb >= 1;
+    if (ewpb >= 1 && lwpb >= 1) {
+      check(cudaFuncSetAttribute(var->eval_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(ewpb * ecoop_warp)), "cudaFuncSetAttribute");
+      check(cudaFuncSetAttribute(var->lsq_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(lwpb * lcoop_warp)), "cudaFuncSetAttribute");
+    }
+    auto launch_heavy = [&]() {
+      if (coop) {
+        const unsigned eb = static_cast<unsigned>((a.n_active + ewpb - 1) / ewpb);
+        const unsigned lb = static_cast<unsigned>((a.n_active + lwpb - 1) / lwpb);
+        check(cudaLaunchKernel(var->eval_coop, dim3(eb), dim3(32 * ewpb), targs, ewpb * ecoop_warp, stream),
+              "launch eval_coop");
+        if (timing_ev) cudaEventRecord(timing_ev[1], stream);
+        check(cudaLaunchKernel(var->lsq_coop, dim3(lb), dim3(32 * lwpb), targs, lwpb * lcoop_warp, stream),
+              "launch lsq_coop");
+      } else {
+        check(cudaLaunchKernel(var->eval_trip, egrid(), dim3(eblock), targs, eval_smem, stream), "launch eval_trip");
+        if (timing_ev) cudaEventRecord(timing_ev[1], stream);
+        check(cudaLaunchKernel(var->lsq_trip, grid, blk, targs, lsq_smem, stream), "launch lsq_trip");
+      }
+    };
     unsigned* busy_slot = busy;
     void* sargs[] = {&a, &busy_slot};
     // seeding pass: every slot takes its first path
@@ -444,6 +491,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
       dev::launch_compaction(m, stream);
       a.n_active = keep;
       grid = dim3(static_cast<unsigned>(keep / tblock));
+      coop = coop || (tail_slots > 0 && ewpb >= 1 && lwpb >= 1 && keep <= tail_slots);
       ++compactions;
       launches += 2;
       return true;
@@ -460,10 +508,12 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
       for (;;) {
         check(cudaMemsetAsync(busy, 0, sizeof(unsigned), stream), "memset busy");
         void* sa[] = {&a, &busy_slot};
+        const size_t trip_active = a.n_active;
+        const bool trip_coop = coop;
         cudaEventRecord(ev[0], stream);
-        check(cudaLaunchKernel(var->eval_trip, egrid(), dim3(eblock), targs, eval_smem, stream), "launch eval_trip");
-        cudaEventRecord(ev[1], stream);
-        check(cudaLaunchKernel(var->lsq_trip, grid, blk, targs, lsq_smem, stream), "launch lsq_trip");
+        timing_ev = ev;
+        launch_heavy();
+        timing_ev = nullptr;
         cudaEventRecord(ev[2], stream);
         check(cudaLaunchKernel(var->step_trip, grid, blk, sa, 0, stream), "launch step_trip");
         cudaEventRecord(ev[3], stream);
@@ -477,8 +527,8 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
           kms[k] += tms[k];
         }
         if (trip_log)
-          std::fprintf(trip_log, "%llu %llu %.4f %.4f %.4f %llu\n", static_cast<unsigned long long>(trips), busy_before,
-                       tms[0], tms[1], tms[2], static_cast<unsigned long long>(a.n_active));
+          std::fprintf(trip_log, "%llu %llu %.4f %.4f %.4f %llu %d\n", static_cast<unsigned long long>(trips), busy_before,
+                       tms[0], tms[1], tms[2], static_cast<unsigned long long>(trip_active), trip_coop ? 1 : 0);
         busy_before = nbusy;
         ++trips;
         launches += 3;
@@ -502,8 +552,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
         for (size_t j = 0; j < graph_trips; ++j) {
           busy_ptrs[j] = busy + j;
           void* sa[] = {&a, &busy_ptrs[j]};
-          check(cudaLaunchKernel(var->eval_trip, egrid(), dim3(eblock), targs, eval_smem, stream), "launch eval_trip");
-          check(cudaLaunchKernel(var->lsq_trip, grid, blk, targs, lsq_smem, stream), "launch lsq_trip");
+          launch_heavy();
           check(cudaLaunchKernel(var->step_trip, grid, blk, sa, 0, stream), "launch step_trip");
         }
         check(cudaStreamEndCapture(stream, &graph), "end capture");

@@ -96,7 +96,12 @@ struct Plan {
   uint64_t cmul_steps = 0;    // complex multiplications in the monomial stage
   uint64_t jac_terms = 0;     // Jacobian contributions (sum of k)
   uint64_t jac_scaled = 0;    // contributions with exponent != 1
+  // warp-cooperative evaluation: term_slot[i] = first contribution slot of term i (n_terms + 1
+  // entries); accumulator a (H_p at a = p, dH_p/dx_v at a = n_polys + p*dim + v) sums the slots
+  // acc_idx[acc_off[a] .. acc_off[a+1]) in that order
+  std::vector<uint32_t> term_slot, acc_off, acc_idx;
   uint32_t n_terms() const { return static_cast<uint32_t>(term_info.size() / 4); }
+  uint32_t n_slots() const { return term_slot.empty() ? 0 : term_slot.back(); }
 };
 
 // build_plan<R>(f, g, gamma) with gamma given as 2L limbs at the plan's level

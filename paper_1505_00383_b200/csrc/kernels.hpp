@@ -23,9 +23,14 @@ struct PlanArgs {
   const uint32_t* pos;
   const uint32_t* base;
   const double* coeff;       // per term: c_start (2L) then c_target (2L)
+  // warp-cooperative evaluation (host.hpp Plan::term_slot / acc_off / acc_idx)
+  const uint32_t* term_slot;
+  const uint32_t* acc_off;
+  const uint32_t* acc_idx;
   int n;                     // variables
   int n_polys;
   int n_terms;
+  int n_slots;               // contribution slots of one evaluation
 };
 
 // One persistent launch of the path tracker.
@@ -93,6 +98,8 @@ struct Variant {
   const void* step_trip;  // __global__ void(TrackArgs, unsigned* busy)
   const void* eval;       // __global__ void(EvalArgs)
   const void* lsq;        // __global__ void(LsqArgs)
+  const void* eval_coop;  // __global__ void(TrackArgs): one warp per slot (tail mode)
+  const void* lsq_coop;   // __global__ void(TrackArgs): one warp per slot (tail mode)
 };
 
 // tail compaction: move the busy slots of [keep, n_active) into idle slots of [0, keep)

@@ -143,6 +143,30 @@ void fill_plan(const System& f, const System* g, const double* gamma_limbs, Plan
   plan.mon_rows = row;
 }
 
+// Tables of the warp-cooperative evaluation (one warp per path): every term's products are
+// computed independently and parked in contribution slots (slot 0: the term's share of H_poly,
+// slots 1..k: its share of dH_poly/dx_var for its k variables in position order); each
+// accumulator (H_p, then dH_p/dx_v at np + p*n + v) then sums its slots in plan order, which is
+// the reference's sum-stage order (evaldiff.cpp:341-373).
+void build_accumulation_lists(Plan& plan) {
+  const uint32_t nt = plan.n_terms(), np = plan.n_polys, n = plan.dim;
+  plan.term_slot.assign(nt + 1, 0);
+  for (uint32_t i = 0; i < nt; ++i) plan.term_slot[i + 1] = plan.term_slot[i] + 1 + plan.term_info[4 * i + 1];
+  const uint32_t n_acc = np + np * n;
+  std::vector<std::vector<uint32_t>> lists(n_acc);
+  for (uint32_t i = 0; i < nt; ++i) {
+    const uint32_t p = plan.term_info[4 * i], k = plan.term_info[4 * i + 1], po = plan.term_info[4 * i + 2];
+    lists[p].push_back(plan.term_slot[i]);
+    for (uint32_t j = 0; j < k; ++j) lists[np + p * n + (plan.pos[po + j] & 0xffffu)].push_back(plan.term_slot[i] + 1 + j);
+  }
+  plan.acc_off.assign(1, 0);
+  plan.acc_idx.clear();
+  for (const auto& l : lists) {
+    plan.acc_idx.insert(plan.acc_idx.end(), l.begin(), l.end());
+    plan.acc_off.push_back(static_cast<uint32_t>(plan.acc_idx.size()));
+  }
+}
+
 }  // namespace
 
 Plan build_plan(const System& f, const System* g, int prec, const double* gamma) {
@@ -168,6 +192,7 @@ Plan build_plan(const System& f, const System* g, int prec, const double* gamma)
     default:
       throw InvalidArgument("build_plan: bad precision");
   }
+  build_accumulation_lists(plan);
   return plan;
 }
 

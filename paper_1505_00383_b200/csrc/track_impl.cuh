@@ -34,9 +34,6 @@
 #ifndef PP_EVAL_MINB
 #define PP_EVAL_MINB 1
 #endif
-#ifndef PP_EVAL_ROLLED
-#define PP_EVAL_ROLLED 1
-#endif
 
 namespace pp {
 namespace dev {
@@ -140,11 +137,106 @@ __device__ __forceinline__ cx<R> ld_flat(const double* p) {
 // (tracker.cpp:488-494).  The coefficient, monomial and sum stages of the reference are fused: the
 // value/derivative slots of one term are produced in registers and accumulated immediately.
 // Because the plan is polynomial-major (evaldiff.cpp:200-236), only one row of H/J is open.
+// One term of the plan at the point X (this thread's column xs): the coefficient, monomial and
+// sum-stage products of evaldiff.cpp:259-374 for term i.  sys_add(v) receives the term's
+// contribution to H_poly (c, or c * value), jac_add(j, var, w) the contribution of its j-th
+// variable to dH_poly/dx_var, in the reference's order.  The Speelpenning prefix stack is a
+// dynamically indexed array (local memory, L1-resident), so the code stays compact for any KMAX.
+template <class R, int KMAX, class SysF, class JacF>
+__device__ __forceinline__ void eval_term(const PlanArgs& pa, int i, const Planar<R>& X, size_t xs, const R& t,
+                                          const R& u, int& poly_out, SysF&& sys_add, JacF&& jac_add) {
+  constexpr int L = level<R>::L;
+  const int4 ti = __ldg(reinterpret_cast<const int4*>(pa.term_info) + i);
+  const int k = ti.y, po = ti.z, nb = ti.w & 0xff, bo = ti.w >> 8;
+  poly_out = ti.x;
+
+  // coefficient stage: c = c_start*(1-t) + c_target*t (evaldiff.cpp:259-274)
+  const double* cp = pa.coeff + static_cast<size_t>(i) * 4 * L;
+  const cx<R> cs = ld_table<R>(cp), ct = ld_table<R>(cp + 2 * L);
+  const cx<R> c{radd(rmul(cs.re, u), rmul(ct.re, t)), radd(rmul(cs.im, u), rmul(ct.im, t))};
+
+  if (k == 0) {  // constants skip the monomial stage (evaldiff.cpp:345-352)
+    sys_add(c);
+    return;
+  }
+
+  // common factor prod x^(e-1) by square-and-multiply (evaldiff.cpp:119-161)
+  cx<R> aux = czero<R>();
+  if (nb > 0) {
+    bool init = false;
+    for (int b = 0; b < nb; ++b) {
+      const uint32_t be = __ldg(pa.base + bo + b);
+      const cx<R> xv = X.ld(static_cast<int>(be & 0xffffu), xs);
+      const uint32_t e = be >> 16;
+      if (e == 1) {
+        aux = init ? cmul(aux, xv) : xv;
+        init = true;
+        continue;
+      }
+      cx<R> sq = xv;
+      for (uint32_t bits = e; bits != 0;) {
+        if (bits & 1u) {
+          aux = init ? cmul(aux, sq) : sq;
+          init = true;
+        }
+        bits >>= 1;
+        if (bits != 0) sq = cmul(sq, sq);
+      }
+    }
+  }
+
+  const uint32_t* pv = pa.pos + po;
+  // derivative contribution w = c*d (scaled by the exponent when e != 1) of variable j
+  auto contribute = [&](int j, cx<R> d) {
+    const uint32_t pe = __ldg(pv + j);
+    if (nb > 0) d = cmul(d, aux);
+    cx<R> w = cmul(c, d);
+    const uint32_t e = pe >> 16;
+    if (e != 1) w = cmuld(w, static_cast<double>(e));
+    jac_add(j, static_cast<int>(pe & 0xffffu), w);
+  };
+
+  if (k == 1) {
+    cx<R> val = X.ld(static_cast<int>(__ldg(pv) & 0xffffu), xs);
+    if (nb > 0) val = cmul(val, aux);
+    sys_add(cmul(c, val));
+    contribute(0, cone<R>());
+    return;
+  }
+
+  // Speelpenning products (evaldiff.cpp:90-115): prefix P_j = x_p0 ... x_p(j-1) for j < k,
+  // value = P_(k-1) x_p(k-1), d_j = P_j * S_(j+1) with the running suffix S.
+  cx<R> P[KMAX > 1 ? KMAX : 2];
+  cx<R> run = X.ld(static_cast<int>(__ldg(pv) & 0xffffu), xs);
+  P[1] = run;
+  for (int j = 2; j < k; ++j) {
+    run = cmul(run, X.ld(static_cast<int>(__ldg(pv + j - 1) & 0xffffu), xs));
+    P[j] = run;
+  }
+  const cx<R> xlast = X.ld(static_cast<int>(__ldg(pv + k - 1) & 0xffffu), xs);
+  cx<R> val = cmul(run, xlast);
+  if (nb > 0) val = cmul(val, aux);
+  sys_add(cmul(c, val));
+  contribute(k - 1, run);  // d_(k-1) = P_(k-1)
+  cx<R> acc = xlast;
+  for (int j = k - 2; j >= 1; --j) {
+    const cx<R> d = cmul(P[j], acc);
+    acc = cmul(acc, X.ld(static_cast<int>(__ldg(pv + j) & 0xffffu), xs));
+    contribute(j, d);
+  }
+  contribute(0, acc);  // d_0 = S_1
+}
+
+// Thread-per-path evaluation.  X: the point (shared memory, this thread's column); JR: open
+// Jacobian row accumulator (shared); outputs: B[p] = -H_p (the least-squares right-hand side,
+// tracker.cpp:249), J[v*n_polys + p]; resid_d = max_p to_double(|H_p|) (tracker.cpp:247-251),
+// resid_r = max_p |H_p| at level R (tracker.cpp:488-494).  The coefficient, monomial and sum
+// stages of the reference are fused per term; because the plan is polynomial-major
+// (evaldiff.cpp:200-236), only one row of H/J is open at a time.
 template <class R, int KMAX>
 __device__ void eval_hj(const PlanArgs& pa, const Planar<R>& X, const Planar<R>& JR, size_t ls,
                         const R& t, const Planar<R>& B, const Planar<R>& J, size_t gs,
                         double& resid_d, R& resid_r) {
-  constexpr int L = level<R>::L;
   const int n = pa.n, np = pa.n_polys;
   const cx<R> zero = czero<R>();
   const R u = rsub(rfrom<R>(1.0), t);  // ws.set_t: 1 - t at level R (evaldiff.hpp:198-201)
@@ -168,119 +260,13 @@ __device__ void eval_hj(const PlanArgs& pa, const Planar<R>& X, const Planar<R>&
   };
 
   for (int i = 0; i < pa.n_terms; ++i) {
-    const int4 ti = __ldg(reinterpret_cast<const int4*>(pa.term_info) + i);
-    const int poly = ti.x, k = ti.y, po = ti.z, nb = ti.w & 0xff, bo = ti.w >> 8;
+    // terms are polynomial-major: close the rows of the polynomials before this term's
+    const int poly = __ldg(pa.term_info + 4 * i);
     while (cur < poly) flush(cur++);
-
-    // coefficient stage: c = c_start*(1-t) + c_target*t (evaldiff.cpp:259-274)
-    const double* cp = pa.coeff + static_cast<size_t>(i) * 4 * L;
-    const cx<R> cs = ld_table<R>(cp), ct = ld_table<R>(cp + 2 * L);
-    const cx<R> c{radd(rmul(cs.re, u), rmul(ct.re, t)), radd(rmul(cs.im, u), rmul(ct.im, t))};
-
-    if (k == 0) {  // constants skip the monomial stage (evaldiff.cpp:345-352)
-      sacc = cadd(sacc, c);
-      continue;
-    }
-
-    // common factor prod x^(e-1) by square-and-multiply (evaldiff.cpp:119-161)
-    cx<R> aux = zero;
-    if (nb > 0) {
-      bool init = false;
-      for (int b = 0; b < nb; ++b) {
-        const uint32_t be = __ldg(pa.base + bo + b);
-        const cx<R> xv = X.ld(static_cast<int>(be & 0xffffu), ls);
-        const uint32_t e = be >> 16;
-        if (e == 1) {
-          aux = init ? cmul(aux, xv) : xv;
-          init = true;
-          continue;
-        }
-        cx<R> sq = xv;
-        for (uint32_t bits = e; bits != 0;) {
-          if (bits & 1u) {
-            aux = init ? cmul(aux, sq) : sq;
-            init = true;
-          }
-          bits >>= 1;
-          if (bits != 0) sq = cmul(sq, sq);
-        }
-      }
-    }
-
-    const uint32_t* pv = pa.pos + po;
-    // derivative contribution w = c*d (scaled by the exponent when e != 1) into row entry var
-    auto contribute = [&](uint32_t pe, cx<R> d) {
-      if (nb > 0) d = cmul(d, aux);
-      cx<R> w = cmul(c, d);
-      const uint32_t e = pe >> 16;
-      if (e != 1) w = cmuld(w, static_cast<double>(e));
-      const int var = static_cast<int>(pe & 0xffffu);
-      JR.st(var, ls, cadd(JR.ld(var, ls), w));
-    };
-
-    if (k == 1) {
-      const uint32_t p0 = __ldg(pv);
-      cx<R> val = X.ld(static_cast<int>(p0 & 0xffffu), ls);
-      if (nb > 0) val = cmul(val, aux);
-      sacc = cadd(sacc, cmul(c, val));
-      contribute(p0, cone<R>());
-      continue;
-    }
-
-    // Speelpenning products (evaldiff.cpp:90-115): prefix P_j = x_p0 ... x_p(j-1) for j < k,
-    // value = P_(k-1) x_p(k-1), d_j = P_j * S_(j+1) with the running suffix S.
-#if PP_EVAL_ROLLED
-    // rolled: the prefix stack is a dynamically indexed (local-memory, L1-resident) array, so
-    // the term loop is compact code whatever KMAX is
-    cx<R> P[KMAX > 1 ? KMAX : 2];
-    cx<R> run = X.ld(static_cast<int>(__ldg(pv) & 0xffffu), ls);
-    P[1] = run;
-    for (int j = 2; j < k; ++j) {
-      run = cmul(run, X.ld(static_cast<int>(__ldg(pv + j - 1) & 0xffffu), ls));
-      P[j] = run;
-    }
-    const uint32_t plast = __ldg(pv + k - 1);
-    const cx<R> xlast = X.ld(static_cast<int>(plast & 0xffffu), ls);
-    cx<R> val = cmul(run, xlast);
-    if (nb > 0) val = cmul(val, aux);
-    sacc = cadd(sacc, cmul(c, val));
-    contribute(plast, run);  // d_(k-1) = P_(k-1)
-    cx<R> acc = xlast;
-    for (int j = k - 2; j >= 1; --j) {
-      const uint32_t pj = __ldg(pv + j);
-      const cx<R> d = cmul(P[j], acc);
-      acc = cmul(acc, X.ld(static_cast<int>(pj & 0xffffu), ls));
-      contribute(pj, d);
-    }
-#else
-    cx<R> P[KMAX > 1 ? KMAX : 2];
-    cx<R> run = X.ld(static_cast<int>(__ldg(pv) & 0xffffu), ls);
-    P[1] = run;
-#pragma unroll
-    for (int j = 2; j < KMAX; ++j) {
-      if (j < k) {
-        run = cmul(run, X.ld(static_cast<int>(__ldg(pv + j - 1) & 0xffffu), ls));
-        P[j] = run;
-      }
-    }
-    const uint32_t plast = __ldg(pv + k - 1);
-    const cx<R> xlast = X.ld(static_cast<int>(plast & 0xffffu), ls);
-    cx<R> val = cmul(run, xlast);
-    if (nb > 0) val = cmul(val, aux);
-    sacc = cadd(sacc, cmul(c, val));
-    contribute(plast, run);  // d_(k-1) = P_(k-1)
-    cx<R> acc = xlast;
-#pragma unroll
-    for (int j = KMAX - 2; j >= 1; --j) {
-      if (j <= k - 2) {
-        const uint32_t pj = __ldg(pv + j);
-        const cx<R> d = cmul(P[j], acc);
-        acc = cmul(acc, X.ld(static_cast<int>(pj & 0xffffu), ls));
-        contribute(pj, d);
-      }
-    }
-#endif
-    contribute(__ldg(pv), acc);  // d_0 = S_1
+    int p_unused;
+    eval_term<R, KMAX>(
+        pa, i, X, ls, t, u, p_unused, [&](const cx<R>& v) { sacc = cadd(sacc, v); },
+        [&](int, int var, const cx<R>& w) { JR.st(var, ls, cadd(JR.ld(var, ls), w)); });
   }
   while (cur < np) flush(cur++);
 }
@@ -791,6 +777,209 @@ __global__ void __launch_bounds__(128) step_trip(const TrackArgs a, unsigned* bu
 }
 
 // ---------------------------------------------------------------------------------------------
+// tail mode: one warp per path slot
+// ---------------------------------------------------------------------------------------------
+// When only a few paths remain (after compaction), a thread per path leaves the GPU idle and each
+// trip costs a lone warp's issue time.  These kernels give each remaining path a whole warp and
+// split its trip across the lanes while keeping the reference's operation order, so results are
+// bitwise those of the thread-per-path kernels:
+//  * evaluation: lanes compute the terms' products independently into contribution slots; each
+//    accumulator (H_p, dH_p/dx_v) then sums its slots in plan order (build_accumulation_lists);
+//  * least squares: lanes own the rows of the Gram-Schmidt column operations (products, axpy,
+//    scaling); every sequential sum of the reference (dot products, norms, back substitution)
+//    is carried out in order by lane 0.
+
+// warp max of a level value (rcmp order; equal values are identical, so the result is exact)
+template <class R>
+__device__ __forceinline__ R warp_rmax(R v) {
+  constexpr int L = level<R>::L;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    R o;
+#pragma unroll
+    for (int l = 0; l < L; ++l) level<R>::set(o, l, __shfl_xor_sync(0xffffffffu, level<R>::get(v, l), off));
+    if (rcmp(o, v) > 0) v = o;
+  }
+  return v;
+}
+__device__ __forceinline__ double warp_fmax(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v = f_max(v, __shfl_xor_sync(0xffffffffu, v, off));
+  return v;
+}
+
+template <class R, int KMAX>
+__global__ void __launch_bounds__(128) eval_coop(const TrackArgs a) {
+  constexpr int L = level<R>::L;
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  const size_t s = static_cast<size_t>(blockIdx.x) * wpb + warp;
+  if (s >= a.n_active) return;  // warp-uniform
+  const SlotInts si{a.si, a.S};
+  const int mode = si(F_MODE, s);
+  if (mode != M_NEWTON && mode != M_REFINE && mode != M_FINAL) return;
+  const PlanArgs& pa = a.plan;
+  const int n = pa.n, np = pa.n_polys;
+  const size_t per_warp = static_cast<size_t>(n + pa.n_slots) * 2 * L;
+  const Planar<R> XS{smem + warp * per_warp, 1}, SL{smem + warp * per_warp + static_cast<size_t>(n) * 2 * L, 1};
+  const Planar<R> X{a.x, a.S}, SR{a.sr, a.S}, J{a.J, a.S}, B{a.B, a.S};
+  for (int v = lane; v < n; v += 32) XS.st(v, 0, X.ld(v, s));
+  __syncwarp();
+  const R t = mode == M_NEWTON ? SR.ldr(R_TNEXT, s) : rfrom<R>(1.0);
+  const R u = rsub(rfrom<R>(1.0), t);
+  for (int i = lane; i < pa.n_terms; i += 32) {
+    const int slot = static_cast<int>(__ldg(pa.term_slot + i));
+    int poly;
+    eval_term<R, KMAX>(
+        pa, i, XS, 0, t, u, poly, [&](const cx<R>& v) { SL.st(slot, 0, v); },
+        [&](int j, int, const cx<R>& w) { SL.st(slot + 1 + j, 0, w); });
+  }
+  __syncwarp();
+  double resid = 0.0;
+  R resid_r = rfrom<R>(0.0);
+  const int n_acc = np + np * n;
+  for (int acc = lane; acc < n_acc; acc += 32) {
+    cx<R> sum = czero<R>();
+    const int e = static_cast<int>(__ldg(pa.acc_off + acc + 1));
+    for (int q = static_cast<int>(__ldg(pa.acc_off + acc)); q < e; ++q)
+      sum = cadd(sum, SL.ld(static_cast<int>(__ldg(pa.acc_idx + q)), 0));
+    if (acc < np) {
+      B.st(acc, s, cneg(sum));
+      const R m = cabsr(sum);
+      resid = f_max(resid, rtod(m));
+      if (rcmp(m, resid_r) > 0) resid_r = m;
+    } else {
+      const int p = (acc - np) / n, v = (acc - np) - p * n;
+      J.st(v * np + p, s, sum);
+    }
+  }
+  resid = warp_fmax(resid);
+  resid_r = warp_rmax<R>(resid_r);
+  if (lane == 0) {
+    a.sd[D_RESID * a.S + s] = resid;
+    SR.str(R_RESID, s, resid_r);
+  }
+}
+
+template <class R>
+__global__ void __launch_bounds__(128) lsq_coop(const TrackArgs a) {
+  constexpr int L = level<R>::L;
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  const size_t s = static_cast<size_t>(blockIdx.x) * wpb + warp;
+  if (s >= a.n_active) return;  // warp-uniform
+  const SlotInts si{a.si, a.S};
+  const int mode = si(F_MODE, s);
+  if (mode != M_NEWTON && mode != M_REFINE) return;
+  const int n = a.plan.n;
+  const int nR = n * (n + 1) / 2;
+  // per warp: Q (n*n), b, R (packed), y, x (the update), and row products P
+  double* base = smem + static_cast<size_t>(warp) * (n * n + 4 * n + nR) * 2 * L;
+  const Planar<R> QS{base, 1}, BS{base + n * n * 2 * L, 1}, RS{base + (n * n + n) * 2 * L, 1},
+      YS{base + (n * n + n + nR) * 2 * L, 1}, DS{base + (n * n + 2 * n + nR) * 2 * L, 1},
+      PS{base + (n * n + 3 * n + nR) * 2 * L, 1};
+  const Planar<R> X{a.x, a.S}, J{a.J, a.S}, B{a.B, a.S};
+  for (int e = lane; e < n * n; e += 32) QS.st(e, 0, J.ld(e, s));
+  for (int e = lane; e < n; e += 32) BS.st(e, 0, B.ld(e, s));
+  __syncwarp();
+  const cx<R> zero = czero<R>();
+
+  // column norms (col_norm, linalg.hpp:57-66): one column per lane, rows in order
+  R max_norm = rfrom<R>(0.0);
+  for (int j = lane; j < n; j += 32) {
+    R acc = rfrom<R>(0.0);
+    for (int r = 0; r < n; ++r) acc = radd(acc, cabs2(QS.ld(j * n + r, 0)));
+    const R nj = rsqrt(acc);
+    if (rcmp(nj, max_norm) > 0) max_norm = nj;
+  }
+  max_norm = warp_rmax<R>(max_norm);
+  const R tol = rmul(max_norm, rfrom<R>(a.rank_tol));
+
+  bool ok = true;
+  for (int k = 0; k < n && ok; ++k) {
+    const int rk = k * (k + 1) / 2;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int i = 0; i < k; ++i) {
+        for (int r = lane; r < n; r += 32) PS.st(r, 0, cmul(cconj(QS.ld(i * n + r, 0)), QS.ld(k * n + r, 0)));
+        __syncwarp();
+        if (lane == 0) {  // dot_conj: rows in order (linalg.hpp:69-73)
+          cx<R> rik = zero;
+          for (int r = 0; r < n; ++r) rik = cadd(rik, PS.ld(r, 0));
+          const cx<R> prev = pass == 0 ? zero : RS.ld(i + rk, 0);
+          RS.st(i + rk, 0, cadd(prev, rik));
+          PS.st(0, 0, rik);
+        }
+        __syncwarp();
+        const cx<R> rik = PS.ld(0, 0);
+        __syncwarp();
+        for (int r = lane; r < n; r += 32) QS.st(k * n + r, 0, csub(QS.ld(k * n + r, 0), cmul(rik, QS.ld(i * n + r, 0))));
+        __syncwarp();
+      }
+    }
+    for (int r = lane; r < n; r += 32) {
+      const R v = cabs2(QS.ld(k * n + r, 0));
+      PS.st(r, 0, cx<R>{v, rfrom<R>(0.0)});
+    }
+    __syncwarp();
+    R rkk = rfrom<R>(0.0);
+    if (lane == 0) {
+      R acc = rfrom<R>(0.0);
+      for (int r = 0; r < n; ++r) acc = radd(acc, PS.ld(r, 0).re);
+      rkk = rsqrt(acc);
+    }
+#pragma unroll
+    for (int l = 0; l < L; ++l) level<R>::set(rkk, l, __shfl_sync(0xffffffffu, level<R>::get(rkk, l), 0));
+    __syncwarp();
+    if (rcmp(rkk, tol) <= 0) {
+      ok = false;
+      break;
+    }
+    const R rinv = rdiv(rfrom<R>(1.0), rkk);  // every lane computes the same value
+    if (lane == 0) RS.st(k + rk, 0, cx<R>{rkk, rfrom<R>(0.0)});
+    for (int r = lane; r < n; r += 32) {
+      const cx<R> q = cmulr(QS.ld(k * n + r, 0), rinv);
+      QS.st(k * n + r, 0, q);
+      PS.st(r, 0, cmul(cconj(q), BS.ld(r, 0)));
+    }
+    __syncwarp();
+    if (lane == 0) {  // y_k = <q_k, b> (linalg.hpp:117)
+      cx<R> y = zero;
+      for (int r = 0; r < n; ++r) y = cadd(y, PS.ld(r, 0));
+      YS.st(k, 0, y);
+    }
+    __syncwarp();
+  }
+  if (lane == 0) si(F_OK, s) = ok ? 1 : 0;
+  if (!ok) return;
+  // back substitution R x = y (linalg.hpp:118-122): products by the lanes, sums in order by lane 0
+  for (int j = n - 1; j >= 0; --j) {
+    for (int i = j + 1 + lane; i < n; i += 32) PS.st(i, 0, cmul(RS.ld(j + i * (i + 1) / 2, 0), DS.ld(i, 0)));
+    __syncwarp();
+    if (lane == 0) {
+      cx<R> acc = YS.ld(j, 0);
+      for (int i = j + 1; i < n; ++i) acc = csub(acc, PS.ld(i, 0));
+      DS.st(j, 0, cdiv(acc, RS.ld(j + j * (j + 1) / 2, 0)));
+    }
+    __syncwarp();
+  }
+  // x += dx; update and iterate norms (tracker.cpp:258-264)
+  double dxn = 0.0, xn = 0.0;
+  for (int v = lane; v < n; v += 32) {
+    const cx<R> dv = DS.ld(v, 0);
+    const cx<R> xv = cadd(X.ld(v, s), dv);
+    X.st(v, s, xv);
+    dxn = f_max(dxn, cabsd(dv));
+    xn = f_max(xn, cabsd(xv));
+  }
+  dxn = warp_fmax(dxn);
+  xn = warp_fmax(xn);
+  if (lane == 0) {
+    a.sd[D_DXN * a.S + s] = dxn;
+    a.sd[D_XN * a.S + s] = xn;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // kernel-level parity entry points
 // ---------------------------------------------------------------------------------------------
 template <class R, int KMAX>
@@ -835,4 +1024,6 @@ __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
    reinterpret_cast<const void*>(&pp::dev::lsq_trip<R>),                          \
    reinterpret_cast<const void*>(&pp::dev::step_trip<R>),                             \
    reinterpret_cast<const void*>(&pp::dev::eval_kernel<R, KM>),                       \
-   reinterpret_cast<const void*>(&pp::dev::lsq_kernel<R>)}
+   reinterpret_cast<const void*>(&pp::dev::lsq_kernel<R>),                       \
+   reinterpret_cast<const void*>(&pp::dev::eval_coop<R, KM>),                        \
+   reinterpret_cast<const void*>(&pp::dev::lsq_coop<R>)}

@@ -87,6 +87,16 @@ def test_track_bitwise(pp, name, system):
     assert_records(sol, g, lo)
 
 
+@pytest.mark.parametrize("name,system", [
+    ("cyclic5_d", "cyclic5"), ("cyclic5_dd", "cyclic5"), ("cyclic5_qd", "cyclic5"), ("cyclic10_dd", "cyclic10"),
+    ("katsura12_qd_mn4", "katsura12"), ("rand32_dd", "rand32"), ("cyclic8_d", "cyclic8"),
+])
+def test_track_bitwise_tail_mode(pp, monkeypatch, name, system):
+    """every trip in tail mode (one warp per path: eval_coop / lsq_coop) gives the same records"""
+    monkeypatch.setenv("PP200_FORCE_COOP", "1")
+    test_track_bitwise(pp, name, system)
+
+
 def test_track_custom_config_bitwise(pp):
     """non-default TrackConfig (failure-heavy): max_newton 2, h_init 0.1, max_steps 40"""
     g = golden("track_cyclic5_d_tight")
