@@ -55,16 +55,21 @@ struct DeviceGuard {
   }
 };
 
+// largest dimension the kernels take at level L: a 32-thread block of the evaluation kernel must
+// hold its point and open Jacobian row (2n complex values per thread) in 200 KB of shared memory
+uint32_t max_dim(int L) { return static_cast<uint32_t>((200 * 1024) / (32 * 2 * 2 * L * sizeof(double))); }
+
 const dev::Variant* pick_variant(int prec, uint32_t n, uint32_t max_k) {
   int count = 0;
   const dev::Variant* v = prec == 0 ? dev::variants_d(&count)
                           : prec == 1 ? dev::variants_dd(&count)
                                       : dev::variants_qd(&count);
+  const int L = prec == 0 ? 1 : (prec == 1 ? 2 : 4);
+  if (n > max_dim(L)) return nullptr;
   const dev::Variant* best = nullptr;
   for (int i = 0; i < count; ++i) {
-    if (v[i].nmax < static_cast<int>(n) || v[i].kmax < static_cast<int>(std::max<uint32_t>(max_k, 2))) continue;
-    if (best == nullptr || v[i].nmax < best->nmax || (v[i].nmax == best->nmax && v[i].kmax < best->kmax))
-      best = &v[i];
+    if (v[i].kmax < static_cast<int>(std::max<uint32_t>(max_k, 2))) continue;
+    if (best == nullptr || v[i].kmax < best->kmax) best = &v[i];
   }
   return best;
 }
@@ -284,7 +289,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   const uint32_t n = plan.dim;
   const uint32_t L = plan.L;
   const dev::Variant* var = pick_variant(plan.prec, n, plan.max_k);
-  if (var == nullptr) throw InvalidArgument("system dimension / monomial size beyond the compiled kernels (n <= 32)");
+  if (var == nullptr) throw InvalidArgument("system dimension / monomial size beyond the compiled kernels (KMAX 16; n <= 97 in dd)");
   const uint64_t count = hi - lo;
 
   cudaDeviceProp prop;
@@ -297,7 +302,8 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   int eblock = static_cast<int>(std::min<size_t>(tblock, std::max<size_t>(32, env_size("PP200_EVAL_BLOCK", tblock))));
   while (tblock % eblock != 0) eblock /= 2;
   const size_t eval_smem = static_cast<size_t>(eblock) * per_thread_smem;
-  const size_t lsq_smem = static_cast<size_t>(tblock) * per_thread_smem / 2;  // the column being orthogonalised
+  // the column being orthogonalised (and, with PP_LSQ_QSMEM, the staged q_i)
+  const size_t lsq_smem = static_cast<size_t>(tblock) * per_thread_smem / 2 * (dev::kLsqQSmem ? 2 : 1);
   check(cudaFuncSetAttribute(var->eval_trip, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(eval_smem)),
         "cudaFuncSetAttribute");
   check(cudaFuncSetAttribute(var->lsq_trip, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsq_smem)),
@@ -426,7 +432,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     cudaEvent_t* timing_ev = nullptr;  // set while per-kernel events are recorded
     void* targs[] = {&a};
 
-    // tail mode (PP200_TAIL_SLOTS, default 8 per SM; 0 disables): once compaction has shrunk the
+    // tail mode (PP200_TAIL_SLOTS, default 32 per SM; 0 disables): once compaction has shrunk the
     // launch to at most that many slots, each remaining path gets a whole warp (eval_coop /
     // lsq_coop), bitwise identical to the thread-per-path kernels
     const size_t el = static_cast<size_t>(2) * L * sizeof(double);  // bytes per complex value
@@ -434,9 +440,12 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     const size_t lcoop_warp = (static_cast<size_t>(n) * n + 4 * n + n * (n + 1) / 2) * el;
     const int ewpb = static_cast<int>(std::min<size_t>(4, (200 * 1024) / ecoop_warp));
     const int lwpb = static_cast<int>(std::min<size_t>(4, (200 * 1024) / lcoop_warp));
-    const size_t tail_slots = env_size("PP200_TAIL_SLOTS", 8 * static_cast<size_t>(prop.multiProcessorCount));
+    const size_t tail_slots = env_size("PP200_TAIL_SLOTS", 32 * static_cast<size_t>(prop.multiProcessorCount));
     // PP200_FORCE_COOP=1 runs every trip in tail mode (used by the parity tests)
-    bool coop = env_size("PP200_FORCE_COOP", 0) != 0 && ewpb >= 1 && lwpb >= 1;
+    // small runs (no more paths than tail slots) start in tail mode: a warp per path spreads a
+    // few thousand paths over every SM instead of packing them into a few blocks
+    bool coop = (env_size("PP200_FORCE_COOP", 0) != 0 || (tail_slots > 0 && count <= tail_slots)) && ewpb >= 1 &&
+                lwpb >= 1;
     if (ewpb >= 1 && lwpb >= 1) {
       check(cudaFuncSetAttribute(var->eval_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(ewpb * ecoop_warp)), "cudaFuncSetAttribute");
@@ -464,13 +473,17 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     check(cudaLaunchKernel(var->step_trip, grid, blk, sargs, 0, stream), "launch step_trip");
     launches = 1;
 
-    // tail compaction once the start counter is exhausted and at most half the launched slots
-    // are busy (PP200_COMPACT=0 disables it)
+    // tail compaction once the start counter is exhausted and at most compact_frac of the
+    // launched slots are busy (PP200_COMPACT=0 disables it)
     const bool compact = env_size("PP200_COMPACT", 1) != 0;
+    // compact when at most this fraction of the launched slots is busy (PP200_COMPACT_PCT)
+    const double compact_frac = static_cast<double>(std::min<size_t>(99, env_size("PP200_COMPACT_PCT", 75))) / 100.0;
     unsigned* holes = nullptr;
     if (compact) check(cudaMallocAsync(reinterpret_cast<void**>(&holes), (2 * S + 2) * sizeof(unsigned), stream), "alloc");
     auto maybe_compact = [&](unsigned long long nbusy, unsigned long long started) -> bool {
-      if (!compact || started < count || nbusy == 0 || nbusy * 2 > a.n_active) return false;
+      if (!compact || started < count || nbusy == 0 ||
+          static_cast<double>(nbusy) > compact_frac * static_cast<double>(a.n_active))
+        return false;
       const size_t keep = (nbusy + tblock - 1) / tblock * tblock;
       if (keep >= a.n_active) return false;
       dev::MoveArgs m{};

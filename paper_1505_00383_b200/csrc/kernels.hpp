@@ -1,8 +1,7 @@
 // kernels.hpp -- argument blocks and the registry of compiled kernel variants.
 //
-// Kernels are templated on the level R (double / dd / qd), NMAX (largest system dimension the
-// register-resident Gram-Schmidt column covers) and KMAX (largest number of distinct variables in
-// a monomial, i.e. the length of the Speelpenning prefix stack kept in registers).  Each
+// Kernels are templated on the level R (double / dd / qd) and KMAX (largest number of distinct
+// variables in a monomial, i.e. the length of the Speelpenning prefix stack).  Each
 // precision's variants live in their own translation unit (track_d.cu, track_dd.cu, track_qd.cu)
 // so they compile in parallel.
 #pragma once
@@ -13,7 +12,12 @@
 namespace pp {
 namespace dev {
 
-constexpr int kHistDepth = 5;  // predictor history depth (reference tracker.cpp:87)
+constexpr int kHistDepth = 5;
+#ifdef PP_LSQ_QSMEM
+constexpr bool kLsqQSmem = PP_LSQ_QSMEM != 0;
+#else
+constexpr bool kLsqQSmem = false;
+#endif  // predictor history depth (reference tracker.cpp:87)
 // slot-state field counts (enums F_*, R_*, D_* in track_impl.cuh)
 constexpr int kIntFields = 14, kRealFields = 4, kDblFields = 3;
 
@@ -92,7 +96,7 @@ struct LsqArgs {
 };
 
 struct Variant {
-  int nmax, kmax;
+  int kmax;
   const void* eval_trip;  // __global__ void(TrackArgs)
   const void* lsq_trip;   // __global__ void(TrackArgs)
   const void* step_trip;  // __global__ void(TrackArgs, unsigned* busy)

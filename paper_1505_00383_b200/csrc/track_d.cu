@@ -5,8 +5,7 @@ namespace pp {
 namespace dev {
 
 static const Variant kVariants[] = {
-    PP_VARIANT(double, 8, 8),   PP_VARIANT(double, 10, 10),
-    PP_VARIANT(double, 16, 4),  PP_VARIANT(double, 32, 4),
+    PP_VARIANT(double, 4), PP_VARIANT(double, 8), PP_VARIANT(double, 10), PP_VARIANT(double, 16),
 };
 
 const Variant* variants_d(int* count) {

@@ -5,8 +5,7 @@ namespace pp {
 namespace dev {
 
 static const Variant kVariants[] = {
-    PP_VARIANT(pp::dd_t, 8, 8),   PP_VARIANT(pp::dd_t, 10, 10),
-    PP_VARIANT(pp::dd_t, 16, 4),  PP_VARIANT(pp::dd_t, 32, 4),
+    PP_VARIANT(pp::dd_t, 4), PP_VARIANT(pp::dd_t, 8), PP_VARIANT(pp::dd_t, 10), PP_VARIANT(pp::dd_t, 16),
 };
 
 const Variant* variants_dd(int* count) {

@@ -19,7 +19,7 @@
 // live in global memory in a slot-minor planar layout (element e, limb-plane p, slot s at
 // ((e*P)+p)*S+s) so a warp's 32 slots touch 32 consecutive doubles -- the paper's transposed
 // layout (Table 5/7).  The Gram-Schmidt column being orthogonalised and the Speelpenning
-// prefix products are register arrays (NMAX / KMAX).
+// prefix stack is a dynamically indexed local array (KMAX).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -294,6 +294,10 @@ __device__ void eval_hj(const PlanArgs& pa, const Planar<R>& X, const Planar<R>&
 #ifndef PP_LSQ_PIPE
 #define PP_LSQ_PIPE 0
 #endif
+// PP_LSQ_QSMEM: q_i staged in shared memory once per projection (doubles the solve's smem)
+#ifndef PP_LSQ_QSMEM
+#define PP_LSQ_QSMEM 0
+#endif
 
 __device__ __forceinline__ void prefetch_line(const double* p) {
 #if PP_LSQ_PREFETCH == 1
@@ -356,6 +360,17 @@ PP_UNROLL_ROWS
           if (r + 1 < n) qn = Q.ld(i * n + r + 1, s);
           C.st(r, cs, csub(C.ld(r, cs), cmul(rik, q)));
         }
+#elif PP_LSQ_QSMEM
+        // stage q_i in shared memory (right after this thread's column): read once from L2/HBM
+        const Planar<R> QI{C.base + static_cast<size_t>(n) * 2 * level<R>::L * C.S, C.S};
+PP_UNROLL_ROWS
+        for (int r = 0; r < n; ++r) QI.st(r, cs, Q.ld(i * n + r, s));
+PP_UNROLL_ROWS
+        for (int r = 0; r < n; ++r) rik = cadd(rik, cmul(cconj(QI.ld(r, cs)), C.ld(r, cs)));
+        const cx<R> prev = pass == 0 ? zero : Rm.ld(i + rk, s);
+        Rm.st(i + rk, s, cadd(prev, rik));
+PP_UNROLL_ROWS
+        for (int r = 0; r < n; ++r) C.st(r, cs, csub(C.ld(r, cs), cmul(rik, QI.ld(r, cs))));
 #else
 PP_UNROLL_ROWS
         for (int r = 0; r < n; ++r) rik = cadd(rik, cmul(cconj(Q.ld(i * n + r, s)), C.ld(r, cs)));
@@ -902,12 +917,13 @@ __global__ void __launch_bounds__(128) lsq_coop(const TrackArgs a) {
       for (int i = 0; i < k; ++i) {
         for (int r = lane; r < n; r += 32) PS.st(r, 0, cmul(cconj(QS.ld(i * n + r, 0)), QS.ld(k * n + r, 0)));
         __syncwarp();
-        if (lane == 0) {  // dot_conj: rows in order (linalg.hpp:69-73)
-          cx<R> rik = zero;
-          for (int r = 0; r < n; ++r) rik = cadd(rik, PS.ld(r, 0));
-          const cx<R> prev = pass == 0 ? zero : RS.ld(i + rk, 0);
-          RS.st(i + rk, 0, cadd(prev, rik));
-          PS.st(0, 0, rik);
+        if (lane < 2) {  // dot_conj: rows in order (linalg.hpp:69-73); lane 0 real, lane 1 imaginary part
+          R acc = rfrom<R>(0.0);
+          for (int r = 0; r < n; ++r) acc = radd(acc, PS.ldr(2 * r + lane, 0));
+          const R prev = pass == 0 ? rfrom<R>(0.0) : RS.ldr(2 * (i + rk) + lane, 0);
+          RS.str(2 * (i + rk) + lane, 0, radd(prev, acc));
+          __syncwarp(0x3u);
+          PS.str(lane, 0, acc);
         }
         __syncwarp();
         const cx<R> rik = PS.ld(0, 0);
@@ -942,10 +958,10 @@ __global__ void __launch_bounds__(128) lsq_coop(const TrackArgs a) {
       PS.st(r, 0, cmul(cconj(q), BS.ld(r, 0)));
     }
     __syncwarp();
-    if (lane == 0) {  // y_k = <q_k, b> (linalg.hpp:117)
-      cx<R> y = zero;
-      for (int r = 0; r < n; ++r) y = cadd(y, PS.ld(r, 0));
-      YS.st(k, 0, y);
+    if (lane < 2) {  // y_k = <q_k, b> (linalg.hpp:117), real / imaginary part
+      R y = rfrom<R>(0.0);
+      for (int r = 0; r < n; ++r) y = radd(y, PS.ldr(2 * r + lane, 0));
+      YS.str(2 * k + lane, 0, y);
     }
     __syncwarp();
   }
@@ -955,11 +971,13 @@ __global__ void __launch_bounds__(128) lsq_coop(const TrackArgs a) {
   for (int j = n - 1; j >= 0; --j) {
     for (int i = j + 1 + lane; i < n; i += 32) PS.st(i, 0, cmul(RS.ld(j + i * (i + 1) / 2, 0), DS.ld(i, 0)));
     __syncwarp();
-    if (lane == 0) {
-      cx<R> acc = YS.ld(j, 0);
-      for (int i = j + 1; i < n; ++i) acc = csub(acc, PS.ld(i, 0));
-      DS.st(j, 0, cdiv(acc, RS.ld(j + j * (j + 1) / 2, 0)));
+    if (lane < 2) {  // real / imaginary part of acc -= R_ji x_i, in order
+      R acc = YS.ldr(2 * j + lane, 0);
+      for (int i = j + 1; i < n; ++i) acc = rsub(acc, PS.ldr(2 * i + lane, 0));
+      PS.str(lane, 0, acc);
     }
+    __syncwarp();
+    if (lane == 0) DS.st(j, 0, cdiv(PS.ld(0, 0), RS.ld(j + j * (j + 1) / 2, 0)));
     __syncwarp();
   }
   // x += dx; update and iterate norms (tracker.cpp:258-264)
@@ -1018,12 +1036,13 @@ __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
 }  // namespace dev
 }  // namespace pp
 
-// instantiate the three kernels of one (level, NMAX, KMAX) variant
-#define PP_VARIANT(R, NM, KM)                                                         \
-  {NM, KM, reinterpret_cast<const void*>(&pp::dev::eval_trip<R, KM>),                 \
-   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R>),                          \
+// instantiate the kernels of one (level, KMAX) variant; KMAX bounds the distinct variables of a
+// monomial (the length of the Speelpenning prefix stack)
+#define PP_VARIANT(R, KM)                                                             \
+  {KM, reinterpret_cast<const void*>(&pp::dev::eval_trip<R, KM>),                     \
+   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R>),                              \
    reinterpret_cast<const void*>(&pp::dev::step_trip<R>),                             \
    reinterpret_cast<const void*>(&pp::dev::eval_kernel<R, KM>),                       \
-   reinterpret_cast<const void*>(&pp::dev::lsq_kernel<R>),                       \
-   reinterpret_cast<const void*>(&pp::dev::eval_coop<R, KM>),                        \
+   reinterpret_cast<const void*>(&pp::dev::lsq_kernel<R>),                            \
+   reinterpret_cast<const void*>(&pp::dev::eval_coop<R, KM>),                         \
    reinterpret_cast<const void*>(&pp::dev::lsq_coop<R>)}
