@@ -202,6 +202,14 @@ int pp_lsq_batch(int prec, uint32_t n, uint32_t batch, const double* a, const do
 int pp_solutions_jsonl(const pp_records* rec, int prec, uint32_t dim, const double* gamma, uint64_t seed,
                        const char* command, double wall_ms, uint64_t batches, uint64_t rounds, char* buf,
                        size_t cap, size_t* needed);
+/*
+ * bench-eval (polypath_main.cpp:284-362): `batch` points and t drawn from the
+ * CLI's splitmix64 stream for `seed`, one evaluation of H and dH/dx per point on the device,
+ * timed over `reps` launches after a warm-up (ms = device time per batch evaluation), and the
+ * CLI's FNV-1a checksum of sys then jac in the reference's planar workspace layout.
+ */
+int pp_bench_eval(const pp_homotopy* h, uint64_t seed, uint32_t batch, uint32_t reps, int device, double* ms,
+                  uint64_t* checksum);
 /* to_decimal of one level value (xprec_io.cpp:31-108, 198-212): 17 / 32 / 64 significant digits */
 int pp_to_decimal(int prec, const double* limbs, char* buf, size_t cap);
 

@@ -161,6 +161,7 @@ _sig("pp_track_all", _i32, _vp, _vp, _P(TrackConfigC), _u64, _u64, _i32, _P(Reco
 _sig("pp_solutions_jsonl", _i32, _vp, _i32, _u32, _vp, _u64, ctypes.c_char_p, _dbl, _u64, _u64, ctypes.c_char_p,
      _sz, _P(_sz))
 _sig("pp_to_decimal", _i32, _i32, _vp, ctypes.c_char_p, _sz)
+_sig("pp_bench_eval", _i32, _vp, _u64, _u32, _u32, _i32, _P(_dbl), _P(_u64))
 _sig("pp_eval_batch", _i32, _vp, _u32, _vp, _vp, _vp, _vp, _i32)
 _sig("pp_lsq_batch", _i32, _i32, _u32, _u32, _vp, _vp, _vp, _vp, _i32)
 _sig("pp_test_arith", _i32, _i32, _i32, _vp, _vp, _vp)
@@ -175,7 +176,7 @@ EXPORTED = [
     "pp_load_start_data", "pp_starts_explicit", "pp_starts_roots", "pp_starts_count", "pp_starts_solution", "pp_starts_free",
     "pp_make_homotopy", "pp_homotopy_info", "pp_homotopy_free", "pp_track_config_defaults",
     "pp_track_config_validate", "pp_track_all", "pp_eval_batch", "pp_lsq_batch", "pp_solutions_jsonl",
-    "pp_to_decimal",
+    "pp_to_decimal", "pp_bench_eval",
 ]
 
 
@@ -529,6 +530,14 @@ def eval_batch(h: Homotopy, points: np.ndarray, t: np.ndarray, device: int = 0):
     jac = np.zeros((B, info["n_polys"] * info["dim"], 2 * L))
     _check(lib.pp_eval_batch(h._h, B, _ptr(points), _ptr(t), _ptr(sys), _ptr(jac), device))
     return sys, jac
+
+
+def bench_eval(h: Homotopy, seed: int, batch: int, reps: int = 10, device: int = 0):
+    """bench-eval (polypath_main.cpp:284-362) on the device: the CLI's points for `seed`, device
+    ms per batch evaluation (mean of `reps` launches), and the CLI's FNV-1a checksum (hex)."""
+    ms, cs = _dbl(), _u64()
+    _check(lib.pp_bench_eval(h._h, seed, batch, reps, device, ctypes.byref(ms), ctypes.byref(cs)))
+    return ms.value, f"{cs.value:016x}"
 
 
 def lsq_batch(prec, a: np.ndarray, b: np.ndarray, device: int = 0):

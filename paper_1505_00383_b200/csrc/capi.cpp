@@ -550,6 +550,49 @@ int pp_solutions_jsonl(const pp_records* rec, int prec, uint32_t dim, const doub
   });
 }
 
+int pp_bench_eval(const pp_homotopy* h, uint64_t seed, uint32_t batch, uint32_t reps, int device, double* ms,
+                  uint64_t* checksum) {
+  return guard([&] {
+    need(h != nullptr && batch > 0 && ms != nullptr && checksum != nullptr, "pp_bench_eval: bad argument");
+    const pp::Plan& plan = h->plan;
+    const uint32_t n = plan.dim, np = plan.n_polys, L = plan.L, w = 2 * L;
+    // points and t exactly as cmd_bench draws them (polypath_main.cpp:299-319): splitmix64 units
+    uint64_t state = seed * 0x9e3779b97f4a7c15ULL + 0x243f6a8885a308d3ULL;
+    auto next_unit = [&state]() {
+      state += 0x9e3779b97f4a7c15ULL;
+      uint64_t z = state;
+      z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+      z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+      z ^= z >> 31;
+      return 2.0 * (static_cast<double>(z >> 11) * 0x1p-53) - 1.0;
+    };
+    std::vector<double> xp(static_cast<size_t>(batch) * n * w, 0.0), tp(static_cast<size_t>(batch) * L, 0.0);
+    for (uint32_t j = 0; j < batch; ++j) {
+      for (uint32_t v = 0; v < n; ++v) {
+        xp[(static_cast<size_t>(v) * w + 0) * batch + j] = next_unit();      // re, limb 0 (R{double})
+        xp[(static_cast<size_t>(v) * w + L) * batch + j] = next_unit();      // im, limb 0
+      }
+      tp[j] = 0.5 * (next_unit() + 1.0);  // R{0.5 * (u + 1)}: limb 0
+    }
+    std::vector<double> sys(static_cast<size_t>(batch) * np * w), jac(static_cast<size_t>(batch) * np * n * w);
+    pp_homotopy* hm = const_cast<pp_homotopy*>(h);
+    *ms = pp::device_bench_eval(plan, hm->on(device), batch, xp.data(), tp.data(), reps, sys.data(), jac.data(), device);
+    // fnv1a over ws.sys.raw() then ws.jac.raw() (polypath_main.cpp:275-282, 341-342)
+    uint64_t hsh = 0xcbf29ce484222325ULL;
+    auto fnv = [&hsh](const std::vector<double>& d) {
+      const unsigned char* p = reinterpret_cast<const unsigned char*>(d.data());
+      for (size_t i = 0; i < d.size() * sizeof(double); ++i) {
+        hsh ^= p[i];
+        hsh *= 0x100000001b3ULL;
+      }
+    };
+    fnv(sys);
+    fnv(jac);
+    *checksum = hsh;
+    return PP_OK;
+  });
+}
+
 int pp_to_decimal(int prec, const double* limbs, char* buf, size_t cap) {
   return guard([&] {
     need(limbs_of(prec) > 0 && limbs != nullptr, "pp_to_decimal: bad argument");

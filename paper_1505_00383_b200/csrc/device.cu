@@ -304,7 +304,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   const size_t eval_smem = static_cast<size_t>(eblock) * per_thread_smem;
   // the column being orthogonalised (and, with PP_LSQ_QSMEM, the staged q_i)
   const size_t lsq_smem = static_cast<size_t>(tblock) * per_thread_smem / 2 * (dev::kLsqQSmem ? 2 : 1);
-  check(cudaFuncSetAttribute(var->eval_trip, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(eval_smem)),
+  check(cudaFuncSetAttribute(var->ctrl_eval_trip, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(eval_smem)),
         "cudaFuncSetAttribute");
   check(cudaFuncSetAttribute(var->lsq_trip, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsq_smem)),
         "cudaFuncSetAttribute");
@@ -316,6 +316,10 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   const size_t S = blocks * tblock;
 
   const size_t cw = 2 * L;  // doubles per complex
+  // planar slot arrays are addressed with 32-bit offsets (track_impl.cuh, Planar::at)
+  if (static_cast<size_t>(dev::kHistDepth) * n * cw * S >= (static_cast<size_t>(1) << 32) ||
+      static_cast<size_t>(n) * n * cw * S >= (static_cast<size_t>(1) << 32))
+    throw InvalidArgument("track_all: slot arrays exceed 2^32 doubles (lower PP200_SLOTS_PER_SM)");
   const size_t nJ = static_cast<size_t>(n) * n, nR = static_cast<size_t>(n) * (n + 1) / 2;
   const size_t kH = dev::kHistDepth;
   const size_t graph_trips = std::max<size_t>(1, env_size("PP200_GRAPH_TRIPS", 16));
@@ -452,32 +456,40 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
       check(cudaFuncSetAttribute(var->lsq_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(lwpb * lcoop_warp)), "cudaFuncSetAttribute");
     }
-    auto launch_heavy = [&]() {
+    // one trip = control (step control, prediction, finalize, refill) followed by the heavy
+    // operation of every busy slot.  Thread-per-path mode fuses the control into the evaluation
+    // kernel (ctrl_eval_trip) and runs lsq_trip; tail mode runs step_trip, eval_coop, lsq_coop.
+    // The control part counts the slots with work in this trip into *busy_ptr.  With events
+    // (instrumented mode) the three phases are bracketed: ev[0] ctrl ev[1] eval ev[2] lsq ev[3].
+    auto launch_trip = [&](unsigned* busy_ptr, cudaEvent_t* ev) {
+      void* args[] = {&a, &busy_ptr};
+      if (ev) cudaEventRecord(ev[0], stream);
       if (coop) {
+        check(cudaLaunchKernel(var->step_trip, grid, blk, args, 0, stream), "launch step_trip");
+        if (ev) cudaEventRecord(ev[1], stream);
         const unsigned eb = static_cast<unsigned>((a.n_active + ewpb - 1) / ewpb);
         const unsigned lb = static_cast<unsigned>((a.n_active + lwpb - 1) / lwpb);
         check(cudaLaunchKernel(var->eval_coop, dim3(eb), dim3(32 * ewpb), targs, ewpb * ecoop_warp, stream),
               "launch eval_coop");
-        if (timing_ev) cudaEventRecord(timing_ev[1], stream);
+        if (ev) cudaEventRecord(ev[2], stream);
         check(cudaLaunchKernel(var->lsq_coop, dim3(lb), dim3(32 * lwpb), targs, lwpb * lcoop_warp, stream),
               "launch lsq_coop");
       } else {
-        check(cudaLaunchKernel(var->eval_trip, egrid(), dim3(eblock), targs, eval_smem, stream), "launch eval_trip");
-        if (timing_ev) cudaEventRecord(timing_ev[1], stream);
+        if (ev) cudaEventRecord(ev[1], stream);
+        check(cudaLaunchKernel(var->ctrl_eval_trip, egrid(), dim3(eblock), args, eval_smem, stream),
+              "launch ctrl_eval_trip");
+        if (ev) cudaEventRecord(ev[2], stream);
         check(cudaLaunchKernel(var->lsq_trip, grid, blk, targs, lsq_smem, stream), "launch lsq_trip");
       }
+      if (ev) cudaEventRecord(ev[3], stream);
+      launches += coop ? 3 : 2;
     };
-    unsigned* busy_slot = busy;
-    void* sargs[] = {&a, &busy_slot};
-    // seeding pass: every slot takes its first path
-    check(cudaLaunchKernel(var->step_trip, grid, blk, sargs, 0, stream), "launch step_trip");
-    launches = 1;
 
     // tail compaction once the start counter is exhausted and at most compact_frac of the
     // launched slots are busy (PP200_COMPACT=0 disables it)
     const bool compact = env_size("PP200_COMPACT", 1) != 0;
     // compact when at most this fraction of the launched slots is busy (PP200_COMPACT_PCT)
-    const double compact_frac = static_cast<double>(std::min<size_t>(99, env_size("PP200_COMPACT_PCT", 75))) / 100.0;
+    const double compact_frac = static_cast<double>(std::min<size_t>(99, env_size("PP200_COMPACT_PCT", 90))) / 100.0;
     unsigned* holes = nullptr;
     if (compact) check(cudaMallocAsync(reinterpret_cast<void**>(&holes), (2 * S + 2) * sizeof(unsigned), stream), "alloc");
     auto maybe_compact = [&](unsigned long long nbusy, unsigned long long started) -> bool {
@@ -514,37 +526,28 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
       // instrumented mode: plain launches bracketed by events, per-kernel device time accumulated
       cudaEvent_t ev[4];
       for (auto& e : ev) cudaEventCreate(&e);
-      // PP200_TRIP_LOG=<file>: one line per trip (trip, busy slots, eval/lsq/step ms)
+      // PP200_TRIP_LOG=<file>: one line per trip (trip, busy slots, eval/lsq/control ms, launched
+      // slots, tail mode)
       const char* log_path = std::getenv("PP200_TRIP_LOG");
       FILE* trip_log = (log_path && *log_path) ? std::fopen(log_path, "a") : nullptr;
-      unsigned long long busy_before = std::min<uint64_t>(S, count);
       for (;;) {
         check(cudaMemsetAsync(busy, 0, sizeof(unsigned), stream), "memset busy");
-        void* sa[] = {&a, &busy_slot};
         const size_t trip_active = a.n_active;
         const bool trip_coop = coop;
-        cudaEventRecord(ev[0], stream);
-        timing_ev = ev;
-        launch_heavy();
-        timing_ev = nullptr;
-        cudaEventRecord(ev[2], stream);
-        check(cudaLaunchKernel(var->step_trip, grid, blk, sa, 0, stream), "launch step_trip");
-        cudaEventRecord(ev[3], stream);
+        launch_trip(busy, ev);
         check(cudaMemcpyAsync(mbox, busy, sizeof(unsigned), cudaMemcpyDeviceToHost, stream), "D2H");
         check(cudaMemcpyAsync(mbox + 1, a.next, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream), "D2H");
         check(cudaStreamSynchronize(stream), "tracker trip");
         const unsigned long long nbusy = *reinterpret_cast<unsigned*>(mbox);
-        float tms[3] = {0, 0, 0};
-        for (int k = 0; k < 3; ++k) {
-          cudaEventElapsedTime(&tms[k], ev[k], ev[k + 1]);
-          kms[k] += tms[k];
-        }
+        float tms[3] = {0, 0, 0};  // ctrl, eval (thread mode: control + evaluation), lsq
+        for (int k = 0; k < 3; ++k) cudaEventElapsedTime(&tms[k], ev[k], ev[k + 1]);
+        kms[0] += tms[1];
+        kms[1] += tms[2];
+        kms[2] += tms[0];
         if (trip_log)
-          std::fprintf(trip_log, "%llu %llu %.4f %.4f %.4f %llu %d\n", static_cast<unsigned long long>(trips), busy_before,
-                       tms[0], tms[1], tms[2], static_cast<unsigned long long>(trip_active), trip_coop ? 1 : 0);
-        busy_before = nbusy;
+          std::fprintf(trip_log, "%llu %llu %.4f %.4f %.4f %llu %d\n", static_cast<unsigned long long>(trips), nbusy,
+                       tms[1], tms[2], tms[0], static_cast<unsigned long long>(trip_active), trip_coop ? 1 : 0);
         ++trips;
-        launches += 3;
         if (nbusy == 0) break;
         maybe_compact(nbusy, mbox[1]);
       }
@@ -561,13 +564,8 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
         graph = nullptr;
         check(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "capture");
         check(cudaMemsetAsync(busy, 0, graph_trips * sizeof(unsigned), stream), "memset busy");
-        std::vector<unsigned*> busy_ptrs(graph_trips);
-        for (size_t j = 0; j < graph_trips; ++j) {
-          busy_ptrs[j] = busy + j;
-          void* sa[] = {&a, &busy_ptrs[j]};
-          launch_heavy();
-          check(cudaLaunchKernel(var->step_trip, grid, blk, sa, 0, stream), "launch step_trip");
-        }
+        for (size_t j = 0; j < graph_trips; ++j) launch_trip(busy + j, nullptr);
+        launches -= (coop ? 3 : 2) * graph_trips;  // counted per graph launch below
         check(cudaStreamEndCapture(stream, &graph), "end capture");
         check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
       };
@@ -578,7 +576,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
         check(cudaMemcpyAsync(mbox + 1, a.next, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream), "D2H");
         check(cudaStreamSynchronize(stream), "tracker trips");
         trips += graph_trips;
-        launches += 3 * graph_trips;
+        launches += (coop ? 3 : 2) * graph_trips;
         const unsigned long long nbusy = *reinterpret_cast<unsigned*>(mbox);
         if (nbusy == 0) break;
         if (maybe_compact(nbusy, mbox[1])) capture();
@@ -716,6 +714,61 @@ void device_eval(const Plan& plan, DevicePlan* dp, uint32_t batch, const double*
           for (size_t q = 0; q < w; ++q)
             jac[((i * np + p) * n + v) * w + q] = hj[((v * np + p) * w + q) * batch + i];
   }
+}
+
+// bench-eval (polypath_main.cpp:284-362) on the device: the evaluation kernel over `batch` points
+// given in the reference's planar layout (points [v][plane][batch], t [plane][batch]), timed with
+// CUDA events over `reps` launches after one warm-up launch; sys [p][plane][batch] and the
+// Jacobian in the reference's row order [p*dim + v][plane][batch] are returned for the checksum.
+double device_bench_eval(const Plan& plan, DevicePlan* dp, uint32_t batch, const double* xp, const double* tp,
+                         uint32_t reps, double* sys, double* jac, int device) {
+  DeviceGuard g(device);
+  const uint32_t n = plan.dim, np = plan.n_polys, L = plan.L, w = 2 * L;
+  const dev::Variant* var = pick_variant(plan.prec, n, plan.max_k);
+  if (var == nullptr) throw InvalidArgument("system beyond the compiled kernels");
+  std::vector<double> xv(xp, xp + static_cast<size_t>(batch) * n * w), tv(tp, tp + static_cast<size_t>(batch) * L);
+  double* dx = upload(xv);
+  double* dt = upload(tv);
+  double* ds = dmalloc<double>(static_cast<size_t>(batch) * np * w);
+  double* dj = dmalloc<double>(static_cast<size_t>(batch) * np * n * w);
+  dev::EvalArgs a{};
+  a.plan = plan_args(plan, dp);
+  a.batch = batch;
+  a.x = dx;
+  a.t = dt;
+  a.sys = ds;
+  a.jac = dj;
+  int block = 128;
+  while (block > 32 && static_cast<size_t>(block) * 2 * n * w * sizeof(double) > 200 * 1024) block /= 2;
+  const size_t smem = static_cast<size_t>(block) * 2 * n * w * sizeof(double);
+  check(cudaFuncSetAttribute(var->eval, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)), "attr");
+  void* args[] = {&a};
+  const dim3 grid((batch + block - 1) / block);
+  check(cudaLaunchKernel(var->eval, grid, dim3(block), args, smem, 0), "launch eval");  // warm-up
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, 0);
+  for (uint32_t r = 0; r < std::max<uint32_t>(reps, 1); ++r)
+    check(cudaLaunchKernel(var->eval, grid, dim3(block), args, smem, 0), "launch eval");
+  cudaEventRecord(e1, 0);
+  check(cudaEventSynchronize(e1), "eval kernel");
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  // eval_kernel returns H (not -H) in sys
+  check(cudaMemcpy(sys, ds, static_cast<size_t>(batch) * np * w * 8, cudaMemcpyDeviceToHost), "D2H");
+  std::vector<double> hj(static_cast<size_t>(batch) * np * n * w);
+  check(cudaMemcpy(hj.data(), dj, hj.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+  for (size_t p = 0; p < np; ++p)
+    for (size_t v = 0; v < n; ++v)
+      std::memcpy(jac + (p * n + v) * w * batch, hj.data() + (v * np + p) * w * batch, w * batch * sizeof(double));
+  cudaFree(dx);
+  cudaFree(dt);
+  cudaFree(ds);
+  cudaFree(dj);
+  return ms / std::max<uint32_t>(reps, 1);
 }
 
 void device_lsq(int prec, uint32_t n, uint32_t batch, const double* a, const double* b, double* x,

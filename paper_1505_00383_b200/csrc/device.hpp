@@ -26,6 +26,10 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
 void device_eval(const Plan& plan, DevicePlan* dp, uint32_t batch, const double* points,
                  const double* t, double* sys, double* jac, int device);
 
+// bench-eval on the device (reference planar layouts); returns ms per evaluation launch
+double device_bench_eval(const Plan& plan, DevicePlan* dp, uint32_t batch, const double* xp, const double* tp,
+                         uint32_t reps, double* sys, double* jac, int device);
+
 // batched least_squares_solve (layouts of pp_lsq_batch)
 void device_lsq(int prec, uint32_t n, uint32_t batch, const double* a, const double* b, double* x,
                 uint8_t* ok, int device);

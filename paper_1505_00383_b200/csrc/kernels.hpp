@@ -97,7 +97,7 @@ struct LsqArgs {
 
 struct Variant {
   int kmax;
-  const void* eval_trip;  // __global__ void(TrackArgs)
+  const void* ctrl_eval_trip;  // __global__ void(TrackArgs, unsigned* busy): control + evaluation
   const void* lsq_trip;   // __global__ void(TrackArgs)
   const void* step_trip;  // __global__ void(TrackArgs, unsigned* busy)
   const void* eval;       // __global__ void(EvalArgs)

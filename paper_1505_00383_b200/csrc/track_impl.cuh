@@ -60,36 +60,45 @@ struct Planar {
     return q;
   }
 
+  // Offsets are formed in 32 bits (one IMAD per element instead of 64-bit multiplies per plane);
+  // device_track checks that every planar array holds fewer than 2^32 doubles.
+  __device__ __forceinline__ const double* at(uint32_t first_plane, size_t s) const {
+    return base + (first_plane * static_cast<uint32_t>(S) + static_cast<uint32_t>(s));
+  }
   __device__ __forceinline__ cx<R> ld(int e, size_t s) const {
     cx<R> z;
-    const double* p = base + (static_cast<size_t>(e) * 2 * L) * S + s;
+    const uint32_t S32 = static_cast<uint32_t>(S);
+    const double* p = at(static_cast<uint32_t>(e) * 2 * L, s);
 #pragma unroll
     for (int l = 0; l < L; ++l) {
-      level<R>::set(z.re, l, p[l * S]);
-      level<R>::set(z.im, l, p[(L + l) * S]);
+      level<R>::set(z.re, l, p[l * S32]);
+      level<R>::set(z.im, l, p[(L + l) * S32]);
     }
     return z;
   }
   __device__ __forceinline__ void st(int e, size_t s, const cx<R>& z) const {
-    double* p = base + (static_cast<size_t>(e) * 2 * L) * S + s;
+    const uint32_t S32 = static_cast<uint32_t>(S);
+    double* p = const_cast<double*>(at(static_cast<uint32_t>(e) * 2 * L, s));
 #pragma unroll
     for (int l = 0; l < L; ++l) {
-      p[l * S] = level<R>::get(z.re, l);
-      p[(L + l) * S] = level<R>::get(z.im, l);
+      p[l * S32] = level<R>::get(z.re, l);
+      p[(L + l) * S32] = level<R>::get(z.im, l);
     }
   }
   // real-valued elements (L planes each)
   __device__ __forceinline__ R ldr(int e, size_t s) const {
     R v;
-    const double* p = base + (static_cast<size_t>(e) * L) * S + s;
+    const uint32_t S32 = static_cast<uint32_t>(S);
+    const double* p = at(static_cast<uint32_t>(e) * L, s);
 #pragma unroll
-    for (int l = 0; l < L; ++l) level<R>::set(v, l, p[l * S]);
+    for (int l = 0; l < L; ++l) level<R>::set(v, l, p[l * S32]);
     return v;
   }
   __device__ __forceinline__ void str(int e, size_t s, const R& v) const {
-    double* p = base + (static_cast<size_t>(e) * L) * S + s;
+    const uint32_t S32 = static_cast<uint32_t>(S);
+    double* p = const_cast<double*>(at(static_cast<uint32_t>(e) * L, s));
 #pragma unroll
-    for (int l = 0; l < L; ++l) p[l * S] = level<R>::get(v, l);
+    for (int l = 0; l < L; ++l) p[l * S32] = level<R>::get(v, l);
   }
 };
 
@@ -282,9 +291,15 @@ __device__ void eval_hj(const PlanArgs& pa, const Planar<R>& X, const Planar<R>&
 #ifndef PP_LSQ_UNROLL
 #define PP_LSQ_UNROLL 2
 #endif
-#define PP_STR_(x) #x
-#define PP_STR(x) PP_STR_(x)
-#define PP_UNROLL_ROWS _Pragma(PP_STR(unroll PP_LSQ_UNROLL))
+#ifndef PP_LSQ_UNROLL_D
+#define PP_LSQ_UNROLL_D 4
+#endif
+// complex double: cheap arithmetic per row, so more rows (loads) in flight per iteration
+template <class R>
+struct RowsUnroll {
+  static constexpr int value = level<R>::L == 1 ? PP_LSQ_UNROLL_D : PP_LSQ_UNROLL;
+};
+#define PP_UNROLL_ROWS _Pragma("unroll (RowsUnroll<R>::value)")
 
 // PP_LSQ_PREFETCH: 0 none, 1 into L1, 2 into L2 (the next column to be read)
 #ifndef PP_LSQ_PREFETCH
@@ -423,34 +438,9 @@ struct SlotInts {
   __device__ __forceinline__ int32_t& operator()(int f, size_t s) const { return base[f * S + s]; }
 };
 
-// ---------------------------------------------------------------------------------------------
-// trip kernel 1: evaluate H and dH/dx at every busy slot's point
-// ---------------------------------------------------------------------------------------------
-template <class R, int KMAX>
-__global__ void __launch_bounds__(128, PP_EVAL_MINB) eval_trip(const TrackArgs a) {
-  constexpr int L = level<R>::L;
-  extern __shared__ double smem[];
-  const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (s >= a.n_active) return;
-  const SlotInts si{a.si, a.S};
-  const int mode = si(F_MODE, s);
-  if (mode != M_NEWTON && mode != M_REFINE && mode != M_FINAL) return;
-  const int n = a.plan.n;
-  const size_t ls = threadIdx.x;
-  const Planar<R> XS{smem, blockDim.x};
-  const Planar<R> JR{smem + static_cast<size_t>(n) * 2 * L * blockDim.x, blockDim.x};
-  const Planar<R> X{a.x, a.S}, SR{a.sr, a.S}, J{a.J, a.S}, B{a.B, a.S};
-  for (int v = 0; v < n; ++v) XS.st(v, ls, X.ld(v, s));
-  const R t = mode == M_NEWTON ? SR.ldr(R_TNEXT, s) : rfrom<R>(1.0);
-  double resid;
-  R resid_r;
-  eval_hj<R, KMAX>(a.plan, XS, JR, ls, t, B, J, s, resid, resid_r);
-  a.sd[D_RESID * a.S + s] = resid;
-  SR.str(R_RESID, s, resid_r);
-}
 
 // ---------------------------------------------------------------------------------------------
-// trip kernel 2: least-squares Newton update for corrector / refinement slots
+// trip kernel 2 (thread per path): least-squares Newton update for corrector / refinement slots
 // ---------------------------------------------------------------------------------------------
 template <class R>
 __global__ void __launch_bounds__(128, PP_LSQ_MINB) lsq_trip(const TrackArgs a) {
@@ -763,7 +753,8 @@ __device__ __forceinline__ int step_slot(const TrackArgs& a, size_t s, const Pla
 }
 
 // ---------------------------------------------------------------------------------------------
-// trip kernel 3: per-path control for every slot
+// control kernel of tail mode (thread per slot; the thread-per-path trips fuse it into
+// ctrl_eval_trip)
 // ---------------------------------------------------------------------------------------------
 template <class R>
 __global__ void __launch_bounds__(128) step_trip(const TrackArgs a, unsigned* busy_out) {
@@ -782,6 +773,57 @@ __global__ void __launch_bounds__(128) step_trip(const TrackArgs a, unsigned* bu
     mode = step_slot<R>(a, s, X, s, ho);
   }
   // every busy slot has exactly one heavy operation pending for the next trip
+  const unsigned busy = __ballot_sync(0xffffffffu, in_range && mode != M_DONE);
+  const unsigned solve = __ballot_sync(0xffffffffu, in_range && (mode == M_NEWTON || mode == M_REFINE));
+  if ((threadIdx.x & 31) == 0 && busy != 0) {
+    atomicAdd(busy_out, static_cast<unsigned>(__popc(busy)));
+    atomicAdd(a.work, static_cast<unsigned long long>(__popc(busy)));
+    atomicAdd(a.work + 1, static_cast<unsigned long long>(__popc(solve)));
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// trip kernel 1 (thread per path): control, then the evaluation of H and dH/dx at the slot's
+// point.  The point is staged in shared memory, the control step (step control, predictor,
+// finalize, refill; tracker.cpp:178-338, 402-509) updates it there, the evaluation reads it, and
+// it is written back for the least-squares kernel.  The control part counts the slots with work
+// in this trip (busy_out) and the evaluations / solves issued (a.work).
+// ---------------------------------------------------------------------------------------------
+template <class R, int KMAX>
+__global__ void __launch_bounds__(128, PP_EVAL_MINB) ctrl_eval_trip(const TrackArgs a, unsigned* busy_out) {
+  constexpr int L = level<R>::L;
+  extern __shared__ double smem[];
+  const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool in_range = s < a.n_active;
+  const int n = a.plan.n;
+  const size_t ls = threadIdx.x;
+  const Planar<R> XS{smem, blockDim.x};
+  const Planar<R> JR{smem + static_cast<size_t>(n) * 2 * L * blockDim.x, blockDim.x};
+  int mode = M_DONE;
+  if (in_range) {
+    const SlotInts si{a.si, a.S};
+    mode = si(F_MODE, s);
+    if (mode != M_DONE) {
+      const Planar<R> X{a.x, a.S}, SR{a.sr, a.S}, J{a.J, a.S}, B{a.B, a.S};
+      for (int v = 0; v < n; ++v) XS.st(v, ls, X.ld(v, s));
+      HeavyOut<R> ho;
+      ho.ok = si(F_OK, s) != 0;
+      ho.resid = a.sd[D_RESID * a.S + s];
+      ho.dxn = a.sd[D_DXN * a.S + s];
+      ho.xn = a.sd[D_XN * a.S + s];
+      ho.resid_r = SR.ldr(R_RESID, s);
+      mode = step_slot<R>(a, s, XS, ls, ho);
+      if (mode == M_NEWTON || mode == M_REFINE || mode == M_FINAL) {
+        const R t = mode == M_NEWTON ? SR.ldr(R_TNEXT, s) : rfrom<R>(1.0);
+        double resid;
+        R resid_r;
+        eval_hj<R, KMAX>(a.plan, XS, JR, ls, t, B, J, s, resid, resid_r);
+        a.sd[D_RESID * a.S + s] = resid;
+        SR.str(R_RESID, s, resid_r);
+        for (int v = 0; v < n; ++v) X.st(v, s, XS.ld(v, ls));
+      }
+    }
+  }
   const unsigned busy = __ballot_sync(0xffffffffu, in_range && mode != M_DONE);
   const unsigned solve = __ballot_sync(0xffffffffu, in_range && (mode == M_NEWTON || mode == M_REFINE));
   if ((threadIdx.x & 31) == 0 && busy != 0) {
@@ -1039,7 +1081,7 @@ __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
 // instantiate the kernels of one (level, KMAX) variant; KMAX bounds the distinct variables of a
 // monomial (the length of the Speelpenning prefix stack)
 #define PP_VARIANT(R, KM)                                                             \
-  {KM, reinterpret_cast<const void*>(&pp::dev::eval_trip<R, KM>),                     \
+  {KM, reinterpret_cast<const void*>(&pp::dev::ctrl_eval_trip<R, KM>),                     \
    reinterpret_cast<const void*>(&pp::dev::lsq_trip<R>),                              \
    reinterpret_cast<const void*>(&pp::dev::step_trip<R>),                             \
    reinterpret_cast<const void*>(&pp::dev::eval_kernel<R, KM>),                       \

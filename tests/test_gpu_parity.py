@@ -50,6 +50,20 @@ def test_eval_bitwise(pp, prec, system):
     assert np.array_equal(jac, g["jac"])
 
 
+def test_bench_eval_checksums(pp):
+    """bench-eval on the device reproduces the reference's checksum (tests/golden/bench_eval.json:
+    the CLI's point stream, the reference eval_system_batch, FNV-1a over the planar workspace)"""
+    import json
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "bench_eval.json")) as fh:
+        cases = json.load(fh)
+    for c in cases:
+        _, _, _, h = homotopy(pp, read(c["system"] + ".sys"), c["prec"], seed=c["gamma_seed"])
+        ms, cs = pp.bench_eval(h, c["seed"], c["batch"], reps=3)
+        assert cs == c["checksum"], c
+        assert ms > 0
+
+
 @pytest.mark.parametrize("prec", ["d", "dd", "qd"])
 @pytest.mark.parametrize("n", [1, 5, 10, 13])
 def test_lsq_bitwise(pp, prec, n):
