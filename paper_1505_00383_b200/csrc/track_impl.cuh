@@ -65,6 +65,8 @@ struct Planar {
   __device__ __forceinline__ const double* at(uint32_t first_plane, size_t s) const {
     return base + (first_plane * static_cast<uint32_t>(S) + static_cast<uint32_t>(s));
   }
+  __device__ __forceinline__ const double& ld_addr(int e, size_t s) const { return *at(static_cast<uint32_t>(e) * 2 * L, s); }
+  __device__ __forceinline__ uint32_t plane_stride() const { return static_cast<uint32_t>(S); }
   __device__ __forceinline__ cx<R> ld(int e, size_t s) const {
     cx<R> z;
     const uint32_t S32 = static_cast<uint32_t>(S);
@@ -99,6 +101,44 @@ struct Planar {
     double* p = const_cast<double*>(at(static_cast<uint32_t>(e) * L, s));
 #pragma unroll
     for (int l = 0; l < L; ++l) p[l * S32] = level<R>::get(v, l);
+  }
+};
+
+// Slot-tiled layout of the solver's working arrays (Jacobian / Q, R, right-hand side, Q^H b): the
+// slots are grouped in tiles of 32 (one warp), and a tile's array is contiguous, element-major,
+// plane by plane: element e, plane p of slot s at ((s/32)*E*P + e*P + p)*32 + s%32 for an array
+// of E complex elements (P = 2L planes).  A warp access is one 256-byte line as in the planar
+// layout, but the element's planes are adjacent lines and all strides are compile-time
+// multiples of 256 bytes (DRAM row locality, little address arithmetic).
+template <class R>
+struct Tiled {
+  static constexpr int L = level<R>::L;
+  double* base;
+  uint32_t E;  // complex elements per slot
+
+  __device__ __forceinline__ double* at(int e, size_t s) const {
+    const uint32_t tile = static_cast<uint32_t>(s) >> 5, lane = static_cast<uint32_t>(s) & 31u;
+    return base + ((tile * E + static_cast<uint32_t>(e)) * (2 * L)) * 32u + lane;
+  }
+  __device__ __forceinline__ const double& ld_addr(int e, size_t s) const { return *at(e, s); }
+  __device__ __forceinline__ uint32_t plane_stride() const { return 32u; }
+  __device__ __forceinline__ cx<R> ld(int e, size_t s) const {
+    cx<R> z;
+    const double* p = at(e, s);
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      level<R>::set(z.re, l, p[l * 32]);
+      level<R>::set(z.im, l, p[(L + l) * 32]);
+    }
+    return z;
+  }
+  __device__ __forceinline__ void st(int e, size_t s, const cx<R>& z) const {
+    double* p = at(e, s);
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      p[l * 32] = level<R>::get(z.re, l);
+      p[(L + l) * 32] = level<R>::get(z.im, l);
+    }
   }
 };
 
@@ -242,9 +282,9 @@ __device__ __forceinline__ void eval_term(const PlanArgs& pa, int i, const Plana
 // resid_r = max_p |H_p| at level R (tracker.cpp:488-494).  The coefficient, monomial and sum
 // stages of the reference are fused per term; because the plan is polynomial-major
 // (evaldiff.cpp:200-236), only one row of H/J is open at a time.
-template <class R, int KMAX>
+template <class R, int KMAX, class GA>
 __device__ void eval_hj(const PlanArgs& pa, const Planar<R>& X, const Planar<R>& JR, size_t ls,
-                        const R& t, const Planar<R>& B, const Planar<R>& J, size_t gs,
+                        const R& t, const GA& B, const GA& J, size_t gs,
                         double& resid_d, R& resid_r) {
   const int n = pa.n, np = pa.n_polys;
   const cx<R> zero = czero<R>();
@@ -310,6 +350,15 @@ struct RowsUnroll {
 #define PP_LSQ_PIPE 0
 #endif
 // PP_LSQ_QSMEM: q_i staged in shared memory once per projection (doubles the solve's smem)
+// PP_SLOT_TILED: the solver's working arrays (J/Q, R, b, Q^H b) in the slot-tiled layout
+#ifndef PP_SLOT_TILED
+#define PP_SLOT_TILED 1
+#endif
+#if PP_SLOT_TILED
+#define PP_WORK(ptr, E) Tiled<R>{(ptr), static_cast<uint32_t>(E)}
+#else
+#define PP_WORK(ptr, E) Planar<R>{(ptr), a.S}
+#endif
 #ifndef PP_LSQ_QSMEM
 #define PP_LSQ_QSMEM 0
 #endif
@@ -324,20 +373,23 @@ __device__ __forceinline__ void prefetch_line(const double* p) {
 #endif
 }
 
-template <class R>
-__device__ __forceinline__ void prefetch_column(const Planar<R>& Q, int col, int n, size_t s) {
+template <class R, class GA>
+__device__ __forceinline__ void prefetch_column(const GA& Q, int col, int n, size_t s) {
 #if PP_LSQ_PREFETCH
   constexpr int L = level<R>::L;
-  const double* p = Q.base + static_cast<size_t>(col) * n * 2 * L * Q.S + s;
-  for (int e = 0; e < n * 2 * L; ++e) prefetch_line(p + static_cast<size_t>(e) * Q.S);
+  for (int e = 0; e < n; ++e) {
+    const double* p = &Q.ld_addr(col * n + e, s);
+#pragma unroll
+    for (int q = 0; q < 2 * L; ++q) prefetch_line(p + q * Q.plane_stride());
+  }
 #else
   (void)Q, (void)col, (void)n, (void)s;
 #endif
 }
 
-template <class R>
-__device__ bool lsq_solve_c(int n, double rank_tol, const Planar<R>& Q, const Planar<R>& Rm,
-                            const Planar<R>& B, const Planar<R>& Y, size_t s, const Planar<R>& C,
+template <class R, class GA>
+__device__ bool lsq_solve_c(int n, double rank_tol, const GA& Q, const GA& Rm, const GA& B, const GA& Y,
+                            size_t s, const Planar<R>& C,
                             size_t cs) {
   const cx<R> zero = czero<R>();
   R max_norm = rfrom<R>(0.0);
@@ -452,7 +504,8 @@ __global__ void __launch_bounds__(128, PP_LSQ_MINB) lsq_trip(const TrackArgs a) 
   const int mode = si(F_MODE, s);
   if (mode != M_NEWTON && mode != M_REFINE) return;
   const int n = a.plan.n;
-  const Planar<R> X{a.x, a.S}, J{a.J, a.S}, Rm{a.Rm, a.S}, B{a.B, a.S}, Y{a.Y, a.S};
+  const Planar<R> X{a.x, a.S};
+  const auto J = PP_WORK(a.J, n * n), Rm = PP_WORK(a.Rm, n * (n + 1) / 2), B = PP_WORK(a.B, n), Y = PP_WORK(a.Y, n);
   const Planar<R> C{smem, blockDim.x};
   const size_t cs = threadIdx.x;
   const bool ok = lsq_solve_c<R>(n, a.rank_tol, J, Rm, B, Y, s, C, cs);
@@ -804,7 +857,8 @@ __global__ void __launch_bounds__(128, PP_EVAL_MINB) ctrl_eval_trip(const TrackA
     const SlotInts si{a.si, a.S};
     mode = si(F_MODE, s);
     if (mode != M_DONE) {
-      const Planar<R> X{a.x, a.S}, SR{a.sr, a.S}, J{a.J, a.S}, B{a.B, a.S};
+      const Planar<R> X{a.x, a.S}, SR{a.sr, a.S};
+      const auto J = PP_WORK(a.J, n * a.plan.n_polys), B = PP_WORK(a.B, a.plan.n_polys);
       for (int v = 0; v < n; ++v) XS.st(v, ls, X.ld(v, s));
       HeavyOut<R> ho;
       ho.ok = si(F_OK, s) != 0;
@@ -879,7 +933,8 @@ __global__ void __launch_bounds__(128) eval_coop(const TrackArgs a) {
   const int n = pa.n, np = pa.n_polys;
   const size_t per_warp = static_cast<size_t>(n + pa.n_slots) * 2 * L;
   const Planar<R> XS{smem + warp * per_warp, 1}, SL{smem + warp * per_warp + static_cast<size_t>(n) * 2 * L, 1};
-  const Planar<R> X{a.x, a.S}, SR{a.sr, a.S}, J{a.J, a.S}, B{a.B, a.S};
+  const Planar<R> X{a.x, a.S}, SR{a.sr, a.S};
+  const auto J = PP_WORK(a.J, n * np), B = PP_WORK(a.B, np);
   for (int v = lane; v < n; v += 32) XS.st(v, 0, X.ld(v, s));
   __syncwarp();
   const R t = mode == M_NEWTON ? SR.ldr(R_TNEXT, s) : rfrom<R>(1.0);
@@ -935,7 +990,8 @@ __global__ void __launch_bounds__(128) lsq_coop(const TrackArgs a) {
   const Planar<R> QS{base, 1}, BS{base + n * n * 2 * L, 1}, RS{base + (n * n + n) * 2 * L, 1},
       YS{base + (n * n + n + nR) * 2 * L, 1}, DS{base + (n * n + 2 * n + nR) * 2 * L, 1},
       PS{base + (n * n + 3 * n + nR) * 2 * L, 1};
-  const Planar<R> X{a.x, a.S}, J{a.J, a.S}, B{a.B, a.S};
+  const Planar<R> X{a.x, a.S};
+  const auto J = PP_WORK(a.J, n * n), B = PP_WORK(a.B, n);
   for (int e = lane; e < n * n; e += 32) QS.st(e, 0, J.ld(e, s));
   for (int e = lane; e < n; e += 32) BS.st(e, 0, B.ld(e, s));
   __syncwarp();

@@ -112,6 +112,9 @@ def main(force=False):
         ("katsura12_qd_mn4", k12, "qd", 1, 0, 4, {"max_newton": 4}, {}),
         ("rand32_d", r32, "d", 1, 0, 128, None, {}),
         ("rand32_dd", r32, "dd", 1, 0, 8, None, {}),
+        ("rand32_qd", r32, "qd", 1, 0, 2, None, {}),
+        ("cyclic8_qd", c8, "qd", 1, 0, 4, None, {}),
+        ("cyclic10_qd", c10, "qd", 1, 2000000, 2000002, None, {}),
     ]
     for name, text, prec, seed, lo, hi, cfg, kw in tracks:
         jobs.append((f"track_{name}", lambda a=(name, text, prec, seed, lo, hi, cfg, kw):

@@ -87,7 +87,7 @@ def system_text(pp, system):
     ("cyclic10_dd", "cyclic10"), ("cyclic10_dd_far", "cyclic10"), ("cyclic5_dd_seed101", "cyclic5"),
     ("cyclic8_d", "cyclic8"), ("cyclic8_dd", "cyclic8"), ("katsura12_d", "katsura12"),
     ("katsura12_dd", "katsura12"), ("katsura12_qd_mn4", "katsura12"), ("rand32_d", "rand32"),
-    ("rand32_dd", "rand32"),
+    ("rand32_dd", "rand32"), ("rand32_qd", "rand32"), ("cyclic8_qd", "cyclic8"), ("cyclic10_qd", "cyclic10"),
 ])
 def test_track_bitwise(pp, name, system):
     g = golden(f"track_{name}")
