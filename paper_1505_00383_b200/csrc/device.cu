@@ -441,7 +441,11 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     // lsq_coop), bitwise identical to the thread-per-path kernels
     const size_t el = static_cast<size_t>(2) * L * sizeof(double);  // bytes per complex value
     const size_t ecoop_warp = (static_cast<size_t>(n) + plan.n_slots()) * el;
-    const size_t lcoop_warp = (static_cast<size_t>(n) * n + 4 * n + n * (n + 1) / 2) * el;
+    // Q and R in shared memory while they take at most 16 KB per warp, else left in the global arrays
+    const bool coop_global = static_cast<size_t>(n) * n * el > 16 * 1024;
+    const void* lsq_coop_fn = coop_global ? var->lsq_coop_g : var->lsq_coop;
+    const size_t lcoop_warp =
+        (coop_global ? static_cast<size_t>(4) * n : static_cast<size_t>(n) * n + 4 * n + n * (n + 1) / 2) * el;
     const int ewpb = static_cast<int>(std::min<size_t>(4, (200 * 1024) / ecoop_warp));
     const int lwpb = static_cast<int>(std::min<size_t>(4, (200 * 1024) / lcoop_warp));
     const size_t tail_slots = env_size("PP200_TAIL_SLOTS", 32 * static_cast<size_t>(prop.multiProcessorCount));
@@ -453,7 +457,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     if (ewpb >= 1 && lwpb >= 1) {
       check(cudaFuncSetAttribute(var->eval_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(ewpb * ecoop_warp)), "cudaFuncSetAttribute");
-      check(cudaFuncSetAttribute(var->lsq_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      check(cudaFuncSetAttribute(lsq_coop_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(lwpb * lcoop_warp)), "cudaFuncSetAttribute");
     }
     // one trip = control (step control, prediction, finalize, refill) followed by the heavy
@@ -472,7 +476,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
         check(cudaLaunchKernel(var->eval_coop, dim3(eb), dim3(32 * ewpb), targs, ewpb * ecoop_warp, stream),
               "launch eval_coop");
         if (ev) cudaEventRecord(ev[2], stream);
-        check(cudaLaunchKernel(var->lsq_coop, dim3(lb), dim3(32 * lwpb), targs, lwpb * lcoop_warp, stream),
+        check(cudaLaunchKernel(lsq_coop_fn, dim3(lb), dim3(32 * lwpb), targs, lwpb * lcoop_warp, stream),
               "launch lsq_coop");
       } else {
         if (ev) cudaEventRecord(ev[1], stream);

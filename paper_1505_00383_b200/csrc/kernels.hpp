@@ -103,7 +103,8 @@ struct Variant {
   const void* eval;       // __global__ void(EvalArgs)
   const void* lsq;        // __global__ void(LsqArgs)
   const void* eval_coop;  // __global__ void(TrackArgs): one warp per slot (tail mode)
-  const void* lsq_coop;   // __global__ void(TrackArgs): one warp per slot (tail mode)
+  const void* lsq_coop;   // __global__ void(TrackArgs): one warp per slot (tail mode), Q in shared memory
+  const void* lsq_coop_g; // the same with Q and R in the global (tiled) arrays, for large n
 };
 
 // tail compaction: move the busy slots of [keep, n_active) into idle slots of [0, keep)

@@ -343,7 +343,7 @@ struct RowsUnroll {
 
 // PP_LSQ_PREFETCH: 0 none, 1 into L1, 2 into L2 (the next column to be read)
 #ifndef PP_LSQ_PREFETCH
-#define PP_LSQ_PREFETCH 1
+#define PP_LSQ_PREFETCH 0
 #endif
 // PP_LSQ_PIPE: software-pipelined row loops (row r+1 of q loaded while row r is computed)
 #ifndef PP_LSQ_PIPE
@@ -973,7 +973,27 @@ __global__ void __launch_bounds__(128) eval_coop(const TrackArgs a) {
   }
 }
 
+// matrix access for the warp-per-path solve: the path's Q and R either staged in shared memory
+// (small n) or left in the slot-tiled global arrays (large n, where a shared-memory copy would
+// leave room for one or two warps per SM)
 template <class R>
+struct CoopMat {
+  Planar<R> sm;  // shared memory copy (stride 1), used when tiled.base == nullptr
+  Tiled<R> tiled;
+  size_t s;
+  __device__ __forceinline__ cx<R> ld(int e) const { return tiled.base ? tiled.ld(e, s) : sm.ld(e, 0); }
+  __device__ __forceinline__ void st(int e, const cx<R>& v) const {
+    if (tiled.base) tiled.st(e, s, v);
+    else sm.st(e, 0, v);
+  }
+};
+
+// Warp-per-path least squares, right-looking: as soon as q_k is final, every later column j
+// receives its first-pass projection on q_k (one lane per column, rows in order); column k's own
+// second pass then runs row-parallel with the sums in order on lanes 0/1.  Each column still
+// sees q_0, q_1, ... in the reference's order in both passes (linalg.hpp:88-100), so the result is
+// bitwise that of lsq_solve_c, with the first pass off the critical path.
+template <class R, bool kGlobalQ>
 __global__ void __launch_bounds__(128) lsq_coop(const TrackArgs a) {
   constexpr int L = level<R>::L;
   extern __shared__ double smem[];
@@ -985,14 +1005,23 @@ __global__ void __launch_bounds__(128) lsq_coop(const TrackArgs a) {
   if (mode != M_NEWTON && mode != M_REFINE) return;
   const int n = a.plan.n;
   const int nR = n * (n + 1) / 2;
-  // per warp: Q (n*n), b, R (packed), y, x (the update), and row products P
-  double* base = smem + static_cast<size_t>(warp) * (n * n + 4 * n + nR) * 2 * L;
-  const Planar<R> QS{base, 1}, BS{base + n * n * 2 * L, 1}, RS{base + (n * n + n) * 2 * L, 1},
-      YS{base + (n * n + n + nR) * 2 * L, 1}, DS{base + (n * n + 2 * n + nR) * 2 * L, 1},
-      PS{base + (n * n + 3 * n + nR) * 2 * L, 1};
+  // per warp in shared memory: b, y, x (the update), row products P [, Q (n*n), R (packed)]
+  const size_t per_warp = static_cast<size_t>(4 * n + (kGlobalQ ? 0 : n * n + nR)) * 2 * L;
+  double* base = smem + static_cast<size_t>(warp) * per_warp;
+  const Planar<R> BS{base, 1}, YS{base + n * 2 * L, 1}, DS{base + 2 * n * 2 * L, 1}, PS{base + 3 * n * 2 * L, 1};
   const Planar<R> X{a.x, a.S};
   const auto J = PP_WORK(a.J, n * n), B = PP_WORK(a.B, n);
-  for (int e = lane; e < n * n; e += 32) QS.st(e, 0, J.ld(e, s));
+  CoopMat<R> Q, RM;
+  Q.s = RM.s = s;
+  if (kGlobalQ) {
+    Q.tiled = Tiled<R>{a.J, static_cast<uint32_t>(n * n)};
+    RM.tiled = Tiled<R>{a.Rm, static_cast<uint32_t>(nR)};
+  } else {
+    Q.tiled.base = RM.tiled.base = nullptr;
+    Q.sm = Planar<R>{base + 4 * n * 2 * L, 1};
+    RM.sm = Planar<R>{base + (4 * n + n * n) * 2 * L, 1};
+    for (int e = lane; e < n * n; e += 32) Q.st(e, J.ld(e, s));
+  }
   for (int e = lane; e < n; e += 32) BS.st(e, 0, B.ld(e, s));
   __syncwarp();
   const cx<R> zero = czero<R>();
@@ -1001,7 +1030,7 @@ __global__ void __launch_bounds__(128) lsq_coop(const TrackArgs a) {
   R max_norm = rfrom<R>(0.0);
   for (int j = lane; j < n; j += 32) {
     R acc = rfrom<R>(0.0);
-    for (int r = 0; r < n; ++r) acc = radd(acc, cabs2(QS.ld(j * n + r, 0)));
+    for (int r = 0; r < n; ++r) acc = radd(acc, cabs2(Q.ld(j * n + r)));
     const R nj = rsqrt(acc);
     if (rcmp(nj, max_norm) > 0) max_norm = nj;
   }
@@ -1009,29 +1038,27 @@ __global__ void __launch_bounds__(128) lsq_coop(const TrackArgs a) {
   const R tol = rmul(max_norm, rfrom<R>(a.rank_tol));
 
   bool ok = true;
-  for (int k = 0; k < n && ok; ++k) {
+  for (int k = 0; k < n; ++k) {
     const int rk = k * (k + 1) / 2;
-    for (int pass = 0; pass < 2; ++pass) {
-      for (int i = 0; i < k; ++i) {
-        for (int r = lane; r < n; r += 32) PS.st(r, 0, cmul(cconj(QS.ld(i * n + r, 0)), QS.ld(k * n + r, 0)));
-        __syncwarp();
-        if (lane < 2) {  // dot_conj: rows in order (linalg.hpp:69-73); lane 0 real, lane 1 imaginary part
-          R acc = rfrom<R>(0.0);
-          for (int r = 0; r < n; ++r) acc = radd(acc, PS.ldr(2 * r + lane, 0));
-          const R prev = pass == 0 ? rfrom<R>(0.0) : RS.ldr(2 * (i + rk) + lane, 0);
-          RS.str(2 * (i + rk) + lane, 0, radd(prev, acc));
-          __syncwarp(0x3u);
-          PS.str(lane, 0, acc);
-        }
-        __syncwarp();
-        const cx<R> rik = PS.ld(0, 0);
-        __syncwarp();
-        for (int r = lane; r < n; r += 32) QS.st(k * n + r, 0, csub(QS.ld(k * n + r, 0), cmul(rik, QS.ld(i * n + r, 0))));
-        __syncwarp();
+    // second pass of column k (its first pass arrived from the right-looking steps below)
+    for (int i = 0; i < k; ++i) {
+      for (int r = lane; r < n; r += 32) PS.st(r, 0, cmul(cconj(Q.ld(i * n + r)), Q.ld(k * n + r)));
+      __syncwarp();
+      if (lane < 2) {  // dot_conj: rows in order (linalg.hpp:69-73); lane 0 real, lane 1 imaginary part
+        R acc = rfrom<R>(0.0);
+        for (int r = 0; r < n; ++r) acc = radd(acc, PS.ldr(2 * r + lane, 0));
+        __syncwarp(0x3u);
+        PS.str(lane, 0, acc);
       }
+      __syncwarp();
+      const cx<R> rik = PS.ld(0, 0);
+      if (lane == 0) RM.st(i + rk, cadd(RM.ld(i + rk), rik));  // R(i,k) += rik (second pass)
+      __syncwarp();
+      for (int r = lane; r < n; r += 32) Q.st(k * n + r, csub(Q.ld(k * n + r), cmul(rik, Q.ld(i * n + r))));
+      __syncwarp();
     }
     for (int r = lane; r < n; r += 32) {
-      const R v = cabs2(QS.ld(k * n + r, 0));
+      const R v = cabs2(Q.ld(k * n + r));
       PS.st(r, 0, cx<R>{v, rfrom<R>(0.0)});
     }
     __syncwarp();
@@ -1049,10 +1076,10 @@ __global__ void __launch_bounds__(128) lsq_coop(const TrackArgs a) {
       break;
     }
     const R rinv = rdiv(rfrom<R>(1.0), rkk);  // every lane computes the same value
-    if (lane == 0) RS.st(k + rk, 0, cx<R>{rkk, rfrom<R>(0.0)});
+    if (lane == 0) RM.st(k + rk, cx<R>{rkk, rfrom<R>(0.0)});
     for (int r = lane; r < n; r += 32) {
-      const cx<R> q = cmulr(QS.ld(k * n + r, 0), rinv);
-      QS.st(k * n + r, 0, q);
+      const cx<R> q = cmulr(Q.ld(k * n + r), rinv);
+      Q.st(k * n + r, q);
       PS.st(r, 0, cmul(cconj(q), BS.ld(r, 0)));
     }
     __syncwarp();
@@ -1061,13 +1088,21 @@ __global__ void __launch_bounds__(128) lsq_coop(const TrackArgs a) {
       for (int r = 0; r < n; ++r) y = radd(y, PS.ldr(2 * r + lane, 0));
       YS.str(2 * k + lane, 0, y);
     }
+    // right-looking first pass: q_k projected out of every later column, one lane per column
+    // (R(k,j) = 0 + r as the reference's out.r.at(i, k) += rik on a zero matrix)
+    for (int j = k + 1 + lane; j < n; j += 32) {
+      cx<R> r = zero;
+      for (int row = 0; row < n; ++row) r = cadd(r, cmul(cconj(Q.ld(k * n + row)), Q.ld(j * n + row)));
+      RM.st(k + j * (j + 1) / 2, cadd(zero, r));
+      for (int row = 0; row < n; ++row) Q.st(j * n + row, csub(Q.ld(j * n + row), cmul(r, Q.ld(k * n + row))));
+    }
     __syncwarp();
   }
   if (lane == 0) si(F_OK, s) = ok ? 1 : 0;
   if (!ok) return;
-  // back substitution R x = y (linalg.hpp:118-122): products by the lanes, sums in order by lane 0
+  // back substitution R x = y (linalg.hpp:118-122): products by the lanes, sums in order by lanes 0/1
   for (int j = n - 1; j >= 0; --j) {
-    for (int i = j + 1 + lane; i < n; i += 32) PS.st(i, 0, cmul(RS.ld(j + i * (i + 1) / 2, 0), DS.ld(i, 0)));
+    for (int i = j + 1 + lane; i < n; i += 32) PS.st(i, 0, cmul(RM.ld(j + i * (i + 1) / 2), DS.ld(i, 0)));
     __syncwarp();
     if (lane < 2) {  // real / imaginary part of acc -= R_ji x_i, in order
       R acc = YS.ldr(2 * j + lane, 0);
@@ -1075,7 +1110,7 @@ __global__ void __launch_bounds__(128) lsq_coop(const TrackArgs a) {
       PS.str(lane, 0, acc);
     }
     __syncwarp();
-    if (lane == 0) DS.st(j, 0, cdiv(PS.ld(0, 0), RS.ld(j + j * (j + 1) / 2, 0)));
+    if (lane == 0) DS.st(j, 0, cdiv(PS.ld(0, 0), RM.ld(j + j * (j + 1) / 2)));
     __syncwarp();
   }
   // x += dx; update and iterate norms (tracker.cpp:258-264)
@@ -1143,4 +1178,5 @@ __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
    reinterpret_cast<const void*>(&pp::dev::eval_kernel<R, KM>),                       \
    reinterpret_cast<const void*>(&pp::dev::lsq_kernel<R>),                            \
    reinterpret_cast<const void*>(&pp::dev::eval_coop<R, KM>),                         \
-   reinterpret_cast<const void*>(&pp::dev::lsq_coop<R>)}
+   reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, false>),                       \
+   reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, true>)}
