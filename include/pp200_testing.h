@@ -24,6 +24,9 @@ int pp_test_parse_decimal(int prec, const char* s, double* out);
 int pp_test_to_decimal(int prec, const double* in, char* buf, size_t cap);
 /* per-term (c_start, c_target) coefficient limbs of a homotopy's plan */
 int pp_test_plan_coeffs(const pp_homotopy* h, double* out, size_t cap);
+/* plan tables: which = 0 term_slot, 1 acc_off, 2 acc_idx (warp-per-path accumulation lists),
+ * 3 pos, 4 term_info; *count = entries (PP_E_CAPACITY when cap is too small) */
+int pp_test_plan_tables(const pp_homotopy* h, int which, uint32_t* out, size_t cap, size_t* count);
 /* measured FP64 pipe throughput of a device (DFMA ops/s), the roofline denominator */
 int pp_fp64_peak(int device, double* ops_per_s);
 /* [mon_steps, cmul_steps, jac_terms, jac_scaled, n_base] of a homotopy's plan */

@@ -168,6 +168,7 @@ _sig("pp_test_arith", _i32, _i32, _i32, _vp, _vp, _vp)
 _sig("pp_test_parse_decimal", _i32, _i32, ctypes.c_char_p, _vp)
 _sig("pp_test_to_decimal", _i32, _i32, _vp, ctypes.c_char_p, _sz)
 _sig("pp_test_plan_coeffs", _i32, _vp, _vp, _sz)
+_sig("pp_test_plan_tables", _i32, _vp, _i32, _vp, _sz, _P(_sz))
 _sig("pp_fp64_peak", _i32, _i32, _P(_dbl))
 
 EXPORTED = [
@@ -372,6 +373,16 @@ class Homotopy:
         out = np.zeros((n, 2, 2 * L))
         _check(lib.pp_test_plan_coeffs(self._h, _ptr(out), out.size))
         return out
+
+
+def plan_table(h: "Homotopy", which: str) -> np.ndarray:
+    """test hook: a plan table (term_slot, acc_off, acc_idx, pos, term_info) as an array"""
+    code = {"term_slot": 0, "acc_off": 1, "acc_idx": 2, "pos": 3, "term_info": 4}[which]
+    cnt = _sz()
+    lib.pp_test_plan_tables(h._h, code, None, 0, ctypes.byref(cnt))
+    out = np.zeros(max(1, cnt.value), dtype=np.uint32)
+    _check(lib.pp_test_plan_tables(h._h, code, _ptr(out), out.size, ctypes.byref(cnt)))
+    return out[: cnt.value]
 
 
 def make_homotopy(f: System, g: System, gamma, prec="dd") -> Homotopy:

@@ -706,4 +706,21 @@ int pp_test_plan_coeffs(const pp_homotopy* h, double* out, size_t cap) {
   return PP_OK;
 }
 
+int pp_test_plan_tables(const pp_homotopy* h, int which, uint32_t* out, size_t cap, size_t* count) {
+  if (h == nullptr || count == nullptr) return PP_E_INVALID;
+  const pp::Plan& p = h->plan;
+  const std::vector<uint32_t>* v = which == 0 ? &p.term_slot : which == 1 ? &p.acc_off : which == 2 ? &p.acc_idx
+                                   : which == 3 ? &p.pos : nullptr;
+  std::vector<uint32_t> ti;
+  if (which == 4) {
+    ti.assign(p.term_info.begin(), p.term_info.end());
+    v = &ti;
+  }
+  if (v == nullptr) return PP_E_INVALID;
+  *count = v->size();
+  if (out == nullptr || cap < v->size()) return PP_E_CAPACITY;
+  std::copy(v->begin(), v->end(), out);
+  return PP_OK;
+}
+
 }  // extern "C"

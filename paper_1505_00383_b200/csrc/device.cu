@@ -74,17 +74,16 @@ const dev::Variant* pick_variant(int prec, uint32_t n, uint32_t max_k) {
   return best;
 }
 
-// grow-only per-device scratch arena
+// grow-only scratch arena per (calling host thread, device): concurrent track_all calls from
+// different host threads (each on its own stream) never share a workspace
 struct Arena {
   void* ptr = nullptr;
   size_t bytes = 0;
 };
-std::mutex g_arena_mu;
-std::map<int, Arena> g_arenas;
+thread_local std::map<int, Arena> t_arenas;
 
 void* arena(int device, size_t bytes) {
-  std::lock_guard<std::mutex> lk(g_arena_mu);
-  Arena& a = g_arenas[device];
+  Arena& a = t_arenas[device];
   if (a.bytes < bytes) {
     if (a.ptr) cudaFree(a.ptr);
     a.ptr = nullptr;

@@ -195,3 +195,29 @@ def test_solutions_jsonl_matches_the_reference_cli_format(pp, oracle_mod):
             for v in range(5):
                 assert recs[i]["x"][v][0] == oracle_mod.ref_to_decimal("dd", g["x"][i, v, :2])
                 assert recs[i]["x"][v][1] == oracle_mod.ref_to_decimal("dd", g["x"][i, v, 2:])
+
+
+@pytest.mark.parametrize("system", ["cyclic5", "cyclic10", "katsura12", "rand32"])
+def test_warp_accumulation_lists(pp, system):
+    """tail-mode tables (plan.cpp build_accumulation_lists): every contribution slot is summed by
+    exactly one accumulator, each accumulator visits its slots in plan (term) order, H_p sums the
+    terms of polynomial p, and dH_p/dx_v sums exactly the terms of p that contain x_v"""
+    f = pp.parse_system(read(system + ".sys"))
+    g, _ = pp.total_degree_start(f, "dd")
+    h = pp.make_homotopy(f, g, pp.random_gamma(1), "dd")
+    ts, off, idx = (pp.plan_table(h, k) for k in ("term_slot", "acc_off", "acc_idx"))
+    ti = pp.plan_table(h, "term_info").reshape(-1, 4)
+    pos = pp.plan_table(h, "pos")
+    n, npoly, nt = f.dim, len(f.degrees), len(ti)
+    assert len(ts) == nt + 1 and ts[-1] == len(idx) and len(off) == npoly + npoly * n + 1
+    assert np.array_equal(np.sort(idx), np.arange(len(idx)))          # a partition of the slots
+    for a in range(len(off) - 1):
+        lst = idx[off[a]:off[a + 1]]
+        assert np.all(np.diff(lst.astype(np.int64)) > 0)              # plan order
+        if a < npoly:
+            want = [ts[i] for i in range(nt) if ti[i, 0] == a]
+        else:
+            p, v = divmod(a - npoly, n)
+            want = [ts[i] + 1 + j for i in range(nt) if ti[i, 0] == p
+                    for j in range(ti[i, 1]) if (pos[ti[i, 2] + j] & 0xFFFF) == v]
+        assert list(lst) == want
