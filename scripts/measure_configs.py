@@ -37,7 +37,7 @@ CONFIGS = [
     ("katsura12_qd", "katsura12", "qd", {"max_newton": 4}, 0, 4096),
     ("rand32_d", "rand32", "d", {}, 0, 65536),
     ("rand32_dd", "rand32", "dd", {}, 0, 65536),
-    ("rand32_qd", "rand32", "qd", {}, 0, 1024),
+    ("rand32_qd", "rand32", "qd", {}, 0, 64),
 ]
 
 
