@@ -300,10 +300,13 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   // and open Jacobian row per thread -- is what limits its occupancy)
   int eblock = static_cast<int>(std::min<size_t>(tblock, std::max<size_t>(32, env_size("PP200_EVAL_BLOCK", tblock))));
   while (tblock % eblock != 0) eblock /= 2;
-  const size_t eval_smem = static_cast<size_t>(eblock) * per_thread_smem;
+  // PP200_TMEM=1: the open Jacobian row in tensor memory (n*4L 32-bit columns per thread, at most 128)
+  const bool tmem = env_size("PP200_TMEM", 0) != 0 && static_cast<size_t>(n) * 4 * L <= 128 && !dev::kEvalJGlobal;
+  const void* ctrl_eval_fn = tmem ? var->ctrl_eval_tmem : var->ctrl_eval_trip;
+  const size_t eval_smem = static_cast<size_t>(eblock) * per_thread_smem / ((dev::kEvalJGlobal || tmem) ? 2 : 1);
   // the column being orthogonalised (and, with PP_LSQ_QSMEM, the staged q_i)
   const size_t lsq_smem = static_cast<size_t>(tblock) * per_thread_smem / 2 * (dev::kLsqQSmem ? 2 : 1);
-  check(cudaFuncSetAttribute(var->ctrl_eval_trip, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(eval_smem)),
+  check(cudaFuncSetAttribute(ctrl_eval_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(eval_smem)),
         "cudaFuncSetAttribute");
   check(cudaFuncSetAttribute(var->lsq_trip, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsq_smem)),
         "cudaFuncSetAttribute");
@@ -432,7 +435,6 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     const dim3 blk(tblock);
     dim3 grid(static_cast<unsigned>(blocks));
     auto egrid = [&]() { return dim3(grid.x * static_cast<unsigned>(tblock / eblock)); };
-    cudaEvent_t* timing_ev = nullptr;  // set while per-kernel events are recorded
     void* targs[] = {&a};
 
     // tail mode (PP200_TAIL_SLOTS, default 32 per SM; 0 disables): once compaction has shrunk the
@@ -479,7 +481,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
               "launch lsq_coop");
       } else {
         if (ev) cudaEventRecord(ev[1], stream);
-        check(cudaLaunchKernel(var->ctrl_eval_trip, egrid(), dim3(eblock), args, eval_smem, stream),
+        check(cudaLaunchKernel(ctrl_eval_fn, egrid(), dim3(eblock), args, eval_smem, stream),
               "launch ctrl_eval_trip");
         if (ev) cudaEventRecord(ev[2], stream);
         check(cudaLaunchKernel(var->lsq_trip, grid, blk, targs, lsq_smem, stream), "launch lsq_trip");

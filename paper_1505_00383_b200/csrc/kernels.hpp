@@ -13,6 +13,11 @@ namespace pp {
 namespace dev {
 
 constexpr int kHistDepth = 5;
+#if defined(PP_EVAL_JGLOBAL) && PP_EVAL_JGLOBAL
+constexpr bool kEvalJGlobal = true;
+#else
+constexpr bool kEvalJGlobal = false;
+#endif
 #ifdef PP_LSQ_QSMEM
 constexpr bool kLsqQSmem = PP_LSQ_QSMEM != 0;
 #else
@@ -105,6 +110,7 @@ struct Variant {
   const void* eval_coop;  // __global__ void(TrackArgs): one warp per slot (tail mode)
   const void* lsq_coop;   // __global__ void(TrackArgs): one warp per slot (tail mode), Q in shared memory
   const void* lsq_coop_g; // the same with Q and R in the global (tiled) arrays, for large n
+  const void* ctrl_eval_tmem;  // ctrl_eval_trip with the open Jacobian row in tensor memory
 };
 
 // tail compaction: move the busy slots of [keep, n_active) into idle slots of [0, keep)

@@ -27,6 +27,12 @@
 #include "kernels.hpp"
 #include "xprec.cuh"
 
+// PP_EVAL_JGLOBAL: the thread-per-path evaluation accumulates dH/dx in the global array instead
+// of an open row in shared memory (half the shared memory per thread)
+#ifndef PP_EVAL_JGLOBAL
+#define PP_EVAL_JGLOBAL 0
+#endif
+
 // register budgets of the trip kernels (minimum resident 128-thread blocks per SM)
 #ifndef PP_LSQ_MINB
 #define PP_LSQ_MINB 3
@@ -276,21 +282,111 @@ __device__ __forceinline__ void eval_term(const PlanArgs& pa, int i, const Plana
   contribute(0, acc);  // d_0 = S_1
 }
 
+// Open Jacobian row accessors for eval_hj: a shared-memory column of this thread, or this
+// thread's lane of tensor memory (TMEM).  The TMEM variant frees the shared memory of the open row
+// (half of the evaluation's) so more warps fit on an SM; its tcgen05.ld/st are warp-collective,
+// which holds because every lane of a warp walks the same plan (the variable index is uniform).
+template <class R>
+struct SmemRow {
+  Planar<R> P;
+  size_t ls;
+  __device__ __forceinline__ cx<R> ld(int v) const { return P.ld(v, ls); }
+  __device__ __forceinline__ void st(int v, const cx<R>& z) const { P.st(v, ls, z); }
+};
+
+template <int W>
+struct TmemIO;
+template <>
+struct TmemIO<4> {
+  static __device__ __forceinline__ void ld(uint32_t a, uint32_t* r) {
+    asm volatile("{\n tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n tcgen05.wait::ld.sync.aligned;\n}"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(a) : "memory");
+  }
+  static __device__ __forceinline__ void st(uint32_t a, const uint32_t* r) {
+    asm volatile("{\n tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};\n tcgen05.wait::st.sync.aligned;\n}"
+                 :: "r"(a), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]) : "memory");
+  }
+};
+template <>
+struct TmemIO<8> {
+  static __device__ __forceinline__ void ld(uint32_t a, uint32_t* r) {
+    asm volatile("{\n tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 " tcgen05.wait::ld.sync.aligned;\n}"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(a) : "memory");
+  }
+  static __device__ __forceinline__ void st(uint32_t a, const uint32_t* r) {
+    asm volatile("{\n tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n"
+                 " tcgen05.wait::st.sync.aligned;\n}"
+                 :: "r"(a), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+  }
+};
+template <>
+struct TmemIO<16> {
+  static __device__ __forceinline__ void ld(uint32_t a, uint32_t* r) {
+    TmemIO<8>::ld(a, r);
+    TmemIO<8>::ld(a + 8, r + 8);
+  }
+  static __device__ __forceinline__ void st(uint32_t a, const uint32_t* r) {
+    TmemIO<8>::st(a, r);
+    TmemIO<8>::st(a + 8, r + 8);
+  }
+};
+
+template <class R>
+struct TmemRow {
+  static constexpr int L = level<R>::L, W = 4 * level<R>::L;  // 32-bit columns per complex value
+  uint32_t base;  // this warp's lane quarter and first column
+  __device__ __forceinline__ cx<R> ld(int v) const {
+    uint32_t r[W];
+    __syncwarp();
+    TmemIO<W>::ld(base + static_cast<uint32_t>(v) * W, r);
+    cx<R> z;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      level<R>::set(z.re, l, __hiloint2double(static_cast<int>(r[2 * l + 1]), static_cast<int>(r[2 * l])));
+      level<R>::set(z.im, l, __hiloint2double(static_cast<int>(r[2 * (L + l) + 1]), static_cast<int>(r[2 * (L + l)])));
+    }
+    return z;
+  }
+  __device__ __forceinline__ void st(int v, const cx<R>& z) const {
+    uint32_t r[W];
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      const double a = level<R>::get(z.re, l), b = level<R>::get(z.im, l);
+      r[2 * l] = static_cast<uint32_t>(__double2loint(a));
+      r[2 * l + 1] = static_cast<uint32_t>(__double2hiint(a));
+      r[2 * (L + l)] = static_cast<uint32_t>(__double2loint(b));
+      r[2 * (L + l) + 1] = static_cast<uint32_t>(__double2hiint(b));
+    }
+    __syncwarp();
+    TmemIO<W>::st(base + static_cast<uint32_t>(v) * W, r);
+  }
+};
+
 // Thread-per-path evaluation.  X: the point (shared memory, this thread's column); JR: open
 // Jacobian row accumulator (shared); outputs: B[p] = -H_p (the least-squares right-hand side,
 // tracker.cpp:249), J[v*n_polys + p]; resid_d = max_p to_double(|H_p|) (tracker.cpp:247-251),
 // resid_r = max_p |H_p| at level R (tracker.cpp:488-494).  The coefficient, monomial and sum
 // stages of the reference are fused per term; because the plan is polynomial-major
 // (evaldiff.cpp:200-236), only one row of H/J is open at a time.
-template <class R, int KMAX, class GA>
-__device__ void eval_hj(const PlanArgs& pa, const Planar<R>& X, const Planar<R>& JR, size_t ls,
+template <class R, int KMAX, class GA, class ROW>
+__device__ void eval_hj(const PlanArgs& pa, const Planar<R>& X, const ROW& JR, size_t ls,
                         const R& t, const GA& B, const GA& J, size_t gs,
                         double& resid_d, R& resid_r) {
   const int n = pa.n, np = pa.n_polys;
   const cx<R> zero = czero<R>();
   const R u = rsub(rfrom<R>(1.0), t);  // ws.set_t: 1 - t at level R (evaldiff.hpp:198-201)
 
-  for (int v = 0; v < n; ++v) JR.st(v, ls, zero);
+#if PP_EVAL_JGLOBAL
+  // the Jacobian accumulates in place in the global (tiled) array: zeroed first, then every
+  // contribution added in plan order -- the same additions as the open-row version
+  (void)JR;
+  for (int e = 0; e < n * np; ++e) J.st(e, gs, zero);
+#else
+  for (int v = 0; v < n; ++v) JR.st(v, zero);
+#endif
   cx<R> sacc = zero;
   resid_d = 0.0;
   resid_r = rfrom<R>(0.0);
@@ -301,10 +397,12 @@ __device__ void eval_hj(const PlanArgs& pa, const Planar<R>& X, const Planar<R>&
     R m = cabsr(sacc);
     resid_d = f_max(resid_d, rtod(m));
     if (rcmp(m, resid_r) > 0) resid_r = m;
+#if !PP_EVAL_JGLOBAL
     for (int v = 0; v < n; ++v) {
-      J.st(v * np + p, gs, JR.ld(v, ls));
-      JR.st(v, ls, zero);
+      J.st(v * np + p, gs, JR.ld(v));
+      JR.st(v, zero);
     }
+#endif
     sacc = zero;
   };
 
@@ -315,7 +413,11 @@ __device__ void eval_hj(const PlanArgs& pa, const Planar<R>& X, const Planar<R>&
     int p_unused;
     eval_term<R, KMAX>(
         pa, i, X, ls, t, u, p_unused, [&](const cx<R>& v) { sacc = cadd(sacc, v); },
-        [&](int, int var, const cx<R>& w) { JR.st(var, ls, cadd(JR.ld(var, ls), w)); });
+#if PP_EVAL_JGLOBAL
+        [&](int, int var, const cx<R>& w) { J.st(var * np + poly, gs, cadd(J.ld(var * np + poly, gs), w)); });
+#else
+        [&](int, int var, const cx<R>& w) { JR.st(var, cadd(JR.ld(var), w)); });
+#endif
   }
   while (cur < np) flush(cur++);
 }
@@ -842,7 +944,7 @@ __global__ void __launch_bounds__(128) step_trip(const TrackArgs a, unsigned* bu
 // it is written back for the least-squares kernel.  The control part counts the slots with work
 // in this trip (busy_out) and the evaluations / solves issued (a.work).
 // ---------------------------------------------------------------------------------------------
-template <class R, int KMAX>
+template <class R, int KMAX, bool kTmem>
 __global__ void __launch_bounds__(128, PP_EVAL_MINB) ctrl_eval_trip(const TrackArgs a, unsigned* busy_out) {
   constexpr int L = level<R>::L;
   extern __shared__ double smem[];
@@ -851,14 +953,33 @@ __global__ void __launch_bounds__(128, PP_EVAL_MINB) ctrl_eval_trip(const TrackA
   const int n = a.plan.n;
   const size_t ls = threadIdx.x;
   const Planar<R> XS{smem, blockDim.x};
-  const Planar<R> JR{smem + static_cast<size_t>(n) * 2 * L * blockDim.x, blockDim.x};
+  // TMEM variant: the CTA's open rows live in tensor memory (warp w: lanes 32*(w%4) .. +31,
+  // columns (w/4) * n*4L ..); one warp allocates, all fence around the barrier
+  __shared__ uint32_t tmem_base;
+  constexpr uint32_t kCols = kTmem ? 128u : 0u;
+  if (kTmem) {
+    if (threadIdx.x < 32) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                       static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base))),
+                   "n"(kCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+  }
+  const int warp = threadIdx.x >> 5;
+  const uint32_t row_base = kTmem ? tmem_base + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
+                                        static_cast<uint32_t>((warp >> 2) * n * 4 * L)
+                                  : 0u;
   int mode = M_DONE;
+  bool need = false;
+  R t = rfrom<R>(1.0);
   if (in_range) {
     const SlotInts si{a.si, a.S};
     mode = si(F_MODE, s);
     if (mode != M_DONE) {
       const Planar<R> X{a.x, a.S}, SR{a.sr, a.S};
-      const auto J = PP_WORK(a.J, n * a.plan.n_polys), B = PP_WORK(a.B, a.plan.n_polys);
       for (int v = 0; v < n; ++v) XS.st(v, ls, X.ld(v, s));
       HeavyOut<R> ho;
       ho.ok = si(F_OK, s) != 0;
@@ -867,16 +988,28 @@ __global__ void __launch_bounds__(128, PP_EVAL_MINB) ctrl_eval_trip(const TrackA
       ho.xn = a.sd[D_XN * a.S + s];
       ho.resid_r = SR.ldr(R_RESID, s);
       mode = step_slot<R>(a, s, XS, ls, ho);
-      if (mode == M_NEWTON || mode == M_REFINE || mode == M_FINAL) {
-        const R t = mode == M_NEWTON ? SR.ldr(R_TNEXT, s) : rfrom<R>(1.0);
-        double resid;
-        R resid_r;
-        eval_hj<R, KMAX>(a.plan, XS, JR, ls, t, B, J, s, resid, resid_r);
-        a.sd[D_RESID * a.S + s] = resid;
-        SR.str(R_RESID, s, resid_r);
-        for (int v = 0; v < n; ++v) X.st(v, s, XS.ld(v, ls));
-      }
+      need = mode == M_NEWTON || mode == M_REFINE || mode == M_FINAL;
+      if (mode == M_NEWTON) t = SR.ldr(R_TNEXT, s);
     }
+  }
+  const auto J = PP_WORK(a.J, n * a.plan.n_polys), B = PP_WORK(a.B, a.plan.n_polys);
+  double resid;
+  R resid_r;
+  if (kTmem) {
+    // warp-collective TMEM accesses: the warp evaluates if any lane needs it; the other lanes
+    // run the same plan on their (unused) point and discard the results
+    if (__any_sync(0xffffffffu, need)) {
+      eval_hj<R, KMAX>(a.plan, XS, TmemRow<R>{row_base}, ls, t, B, J, s, resid, resid_r);
+    }
+  } else if (need) {
+    const Planar<R> JR{smem + static_cast<size_t>(n) * 2 * L * blockDim.x, blockDim.x};
+    eval_hj<R, KMAX>(a.plan, XS, SmemRow<R>{JR, ls}, ls, t, B, J, s, resid, resid_r);
+  }
+  if (need) {
+    const Planar<R> X{a.x, a.S}, SR{a.sr, a.S};
+    a.sd[D_RESID * a.S + s] = resid;
+    SR.str(R_RESID, s, resid_r);
+    for (int v = 0; v < n; ++v) X.st(v, s, XS.ld(v, ls));
   }
   const unsigned busy = __ballot_sync(0xffffffffu, in_range && mode != M_DONE);
   const unsigned solve = __ballot_sync(0xffffffffu, in_range && (mode == M_NEWTON || mode == M_REFINE));
@@ -884,6 +1017,13 @@ __global__ void __launch_bounds__(128, PP_EVAL_MINB) ctrl_eval_trip(const TrackA
     atomicAdd(busy_out, static_cast<unsigned>(__popc(busy)));
     atomicAdd(a.work, static_cast<unsigned long long>(__popc(busy)));
     atomicAdd(a.work + 1, static_cast<unsigned long long>(__popc(solve)));
+  }
+  if (kTmem) {
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    if (threadIdx.x < 32)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "n"(kCols));
   }
 }
 
@@ -1149,7 +1289,7 @@ __global__ void __launch_bounds__(128) eval_kernel(const EvalArgs a) {
   const Planar<R> B{a.sys, a.batch}, J{a.jac, a.batch};
   double rd;
   R rr;
-  eval_hj<R, KMAX>(a.plan, X, JR, ls, t, B, J, s, rd, rr);
+  eval_hj<R, KMAX>(a.plan, X, SmemRow<R>{JR, ls}, ls, t, B, J, s, rd, rr);
   // B holds -H; return H
   for (int p = 0; p < a.plan.n_polys; ++p) B.st(p, s, cneg(B.ld(p, s)));
 }
@@ -1172,11 +1312,12 @@ __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
 // instantiate the kernels of one (level, KMAX) variant; KMAX bounds the distinct variables of a
 // monomial (the length of the Speelpenning prefix stack)
 #define PP_VARIANT(R, KM)                                                             \
-  {KM, reinterpret_cast<const void*>(&pp::dev::ctrl_eval_trip<R, KM>),                     \
+  {KM, reinterpret_cast<const void*>(&pp::dev::ctrl_eval_trip<R, KM, false>),                     \
    reinterpret_cast<const void*>(&pp::dev::lsq_trip<R>),                              \
    reinterpret_cast<const void*>(&pp::dev::step_trip<R>),                             \
    reinterpret_cast<const void*>(&pp::dev::eval_kernel<R, KM>),                       \
    reinterpret_cast<const void*>(&pp::dev::lsq_kernel<R>),                            \
    reinterpret_cast<const void*>(&pp::dev::eval_coop<R, KM>),                         \
    reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, false>),                       \
-   reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, true>)}
+   reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, true>),                        \
+   reinterpret_cast<const void*>(&pp::dev::ctrl_eval_trip<R, KM, true>)}

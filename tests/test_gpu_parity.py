@@ -105,14 +105,17 @@ def test_track_bitwise(pp, name, system):
     ("cyclic5_d", "cyclic5"), ("cyclic5_dd", "cyclic5"), ("cyclic5_qd", "cyclic5"), ("cyclic10_dd", "cyclic10"),
     ("katsura12_qd_mn4", "katsura12"), ("rand32_dd", "rand32"), ("cyclic8_d", "cyclic8"),
 ])
-@pytest.mark.parametrize("mode", ["warp_per_path", "thread_per_path"])
+@pytest.mark.parametrize("mode", ["warp_per_path", "thread_per_path", "thread_per_path_tmem"])
 def test_track_bitwise_modes(pp, monkeypatch, name, system, mode):
-    """both engines give the reference records: every trip in tail mode (a warp per path:
-    eval_coop / lsq_coop), or never (a thread per path; small runs otherwise start in tail mode)"""
+    """every engine gives the reference records: every trip in tail mode (a warp per path:
+    eval_coop / lsq_coop), or never (a thread per path; small runs otherwise start in tail mode),
+    also with the open Jacobian row in tensor memory (PP200_TMEM)"""
     if mode == "warp_per_path":
         monkeypatch.setenv("PP200_FORCE_COOP", "1")
     else:
         monkeypatch.setenv("PP200_TAIL_SLOTS", "0")
+    if mode.endswith("tmem"):
+        monkeypatch.setenv("PP200_TMEM", "1")
     test_track_bitwise(pp, name, system)
 
 
