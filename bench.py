@@ -45,6 +45,9 @@ def chunk_offset(c: int, count: int, B: int) -> int:
 
 
 def dist_setup():
+    """One process per GPU (torchrun).  The data path has no collective; torch.distributed only
+    carries the barrier and the max-over-ranks timing.  PP200_DIST_BACKEND=gloo (with more ranks
+    than GPUs, ranks share devices round-robin) exercises the multi-rank logic on one GPU."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -53,8 +56,9 @@ def dist_setup():
         import torch
         import torch.distributed as dist
 
+        local = local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("PP200_DIST_BACKEND", "nccl"))
     return world, rank, local, dist
 
 
@@ -71,7 +75,8 @@ def max_over_ranks(dist, local, value: float) -> float:
         return value
     import torch
 
-    t = torch.tensor([value], dtype=torch.float64, device=f"cuda:{local}")
+    dev = f"cuda:{local}" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([value], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 

@@ -300,8 +300,11 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   // and open Jacobian row per thread -- is what limits its occupancy)
   int eblock = static_cast<int>(std::min<size_t>(tblock, std::max<size_t>(32, env_size("PP200_EVAL_BLOCK", tblock))));
   while (tblock % eblock != 0) eblock /= 2;
-  // PP200_TMEM=1: the open Jacobian row in tensor memory (n*4L 32-bit columns per thread, at most 128)
-  const bool tmem = env_size("PP200_TMEM", 0) != 0 && static_cast<size_t>(n) * 4 * L <= 128 && !dev::kEvalJGlobal;
+  // the open Jacobian row in tensor memory (n*4L 32-bit columns per thread, at most 128; a CTA of
+  // four warps covers the four TMEM lane quarters, four CTAs use all 512 columns); PP200_TMEM=0
+  // keeps it in shared memory
+  const bool tmem = env_size("PP200_TMEM", 1) != 0 && static_cast<size_t>(n) * 4 * L <= 128 && eblock == 128 &&
+                    !dev::kEvalJGlobal;
   const void* ctrl_eval_fn = tmem ? var->ctrl_eval_tmem : var->ctrl_eval_trip;
   const size_t eval_smem = static_cast<size_t>(eblock) * per_thread_smem / ((dev::kEvalJGlobal || tmem) ? 2 : 1);
   // the column being orthogonalised (and, with PP_LSQ_QSMEM, the staged q_i)

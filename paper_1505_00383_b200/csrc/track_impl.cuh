@@ -944,8 +944,8 @@ __global__ void __launch_bounds__(128) step_trip(const TrackArgs a, unsigned* bu
 // it is written back for the least-squares kernel.  The control part counts the slots with work
 // in this trip (busy_out) and the evaluations / solves issued (a.work).
 // ---------------------------------------------------------------------------------------------
-template <class R, int KMAX, bool kTmem>
-__global__ void __launch_bounds__(128, PP_EVAL_MINB) ctrl_eval_trip(const TrackArgs a, unsigned* busy_out) {
+template <class R, int KMAX, bool kTmem, int kMinBlocks>
+__global__ void __launch_bounds__(128, kMinBlocks) ctrl_eval_trip(const TrackArgs a, unsigned* busy_out) {
   constexpr int L = level<R>::L;
   extern __shared__ double smem[];
   const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1312,7 +1312,7 @@ __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
 // instantiate the kernels of one (level, KMAX) variant; KMAX bounds the distinct variables of a
 // monomial (the length of the Speelpenning prefix stack)
 #define PP_VARIANT(R, KM)                                                             \
-  {KM, reinterpret_cast<const void*>(&pp::dev::ctrl_eval_trip<R, KM, false>),                     \
+  {KM, reinterpret_cast<const void*>(&pp::dev::ctrl_eval_trip<R, KM, false, PP_EVAL_MINB>),                     \
    reinterpret_cast<const void*>(&pp::dev::lsq_trip<R>),                              \
    reinterpret_cast<const void*>(&pp::dev::step_trip<R>),                             \
    reinterpret_cast<const void*>(&pp::dev::eval_kernel<R, KM>),                       \
@@ -1320,4 +1320,4 @@ __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
    reinterpret_cast<const void*>(&pp::dev::eval_coop<R, KM>),                         \
    reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, false>),                       \
    reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, true>),                        \
-   reinterpret_cast<const void*>(&pp::dev::ctrl_eval_trip<R, KM, true>)}
+   reinterpret_cast<const void*>(&pp::dev::ctrl_eval_trip<R, KM, true, (sizeof(R) < 32 ? 4 : 1)>)}
