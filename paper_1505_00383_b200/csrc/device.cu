@@ -307,11 +307,20 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
                     !dev::kEvalJGlobal;
   const void* ctrl_eval_fn = tmem ? var->ctrl_eval_tmem : var->ctrl_eval_trip;
   const size_t eval_smem = static_cast<size_t>(eblock) * per_thread_smem / ((dev::kEvalJGlobal || tmem) ? 2 : 1);
-  // the column being orthogonalised (and, with PP_LSQ_QSMEM, the staged q_i)
-  const size_t lsq_smem = static_cast<size_t>(tblock) * per_thread_smem / 2 * (dev::kLsqQSmem ? 2 : 1);
+  // least squares: the column being orthogonalised in shared memory, or (PP200_LSQ_TMEM=1, n*4L <= 128)
+  // in tensor memory with 256-thread CTAs, two per SM (256 TMEM columns each), leaving L1 to Q
+  bool lsq_tm = env_size("PP200_LSQ_TMEM", 0) != 0 && static_cast<size_t>(n) * 4 * L <= 128 && tblock == 128;
+  if (lsq_tm) {
+    int per_sm = 0;
+    check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var->lsq_tmem, 256, 0), "occupancy");
+    lsq_tm = per_sm <= 2;  // more resident CTAs than TMEM columns would stall in tcgen05.alloc
+  }
+  const void* lsq_fn = lsq_tm ? var->lsq_tmem : var->lsq_trip;
+  const int lblock = lsq_tm ? 256 : tblock;
+  const size_t lsq_smem = lsq_tm ? 0 : static_cast<size_t>(tblock) * per_thread_smem / 2;
   check(cudaFuncSetAttribute(ctrl_eval_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(eval_smem)),
         "cudaFuncSetAttribute");
-  check(cudaFuncSetAttribute(var->lsq_trip, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsq_smem)),
+  check(cudaFuncSetAttribute(lsq_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsq_smem)),
         "cudaFuncSetAttribute");
   // slots: PP200_SLOTS_PER_SM (default 512) per SM, never more than the paths (whole blocks)
   const size_t per_sm = std::max<size_t>(tblock, env_size("PP200_SLOTS_PER_SM", 512));
@@ -487,7 +496,9 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
         check(cudaLaunchKernel(ctrl_eval_fn, egrid(), dim3(eblock), args, eval_smem, stream),
               "launch ctrl_eval_trip");
         if (ev) cudaEventRecord(ev[2], stream);
-        check(cudaLaunchKernel(var->lsq_trip, grid, blk, targs, lsq_smem, stream), "launch lsq_trip");
+        check(cudaLaunchKernel(lsq_fn, dim3(static_cast<unsigned>((a.n_active + lblock - 1) / lblock)), dim3(lblock), targs,
+                               lsq_smem, stream),
+              "launch lsq_trip");
       }
       if (ev) cudaEventRecord(ev[3], stream);
       launches += coop ? 3 : 2;

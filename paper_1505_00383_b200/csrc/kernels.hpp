@@ -12,17 +12,12 @@
 namespace pp {
 namespace dev {
 
-constexpr int kHistDepth = 5;
+constexpr int kHistDepth = 5;  // predictor history depth (reference tracker.cpp:87)
 #if defined(PP_EVAL_JGLOBAL) && PP_EVAL_JGLOBAL
-constexpr bool kEvalJGlobal = true;
+constexpr bool kEvalJGlobal = true;  // experiment: dH/dx accumulated in global memory
 #else
 constexpr bool kEvalJGlobal = false;
 #endif
-#ifdef PP_LSQ_QSMEM
-constexpr bool kLsqQSmem = PP_LSQ_QSMEM != 0;
-#else
-constexpr bool kLsqQSmem = false;
-#endif  // predictor history depth (reference tracker.cpp:87)
 // slot-state field counts (enums F_*, R_*, D_* in track_impl.cuh)
 constexpr int kIntFields = 14, kRealFields = 4, kDblFields = 3;
 
@@ -111,6 +106,7 @@ struct Variant {
   const void* lsq_coop;   // __global__ void(TrackArgs): one warp per slot (tail mode), Q in shared memory
   const void* lsq_coop_g; // the same with Q and R in the global (tiled) arrays, for large n
   const void* ctrl_eval_tmem;  // ctrl_eval_trip with the open Jacobian row in tensor memory
+  const void* lsq_tmem;        // lsq_trip with the Gram-Schmidt column in tensor memory
 };
 
 // tail compaction: move the busy slots of [keep, n_active) into idle slots of [0, keep)

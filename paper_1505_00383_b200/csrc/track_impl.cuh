@@ -447,11 +447,7 @@ struct RowsUnroll {
 #ifndef PP_LSQ_PREFETCH
 #define PP_LSQ_PREFETCH 0
 #endif
-// PP_LSQ_PIPE: software-pipelined row loops (row r+1 of q loaded while row r is computed)
-#ifndef PP_LSQ_PIPE
-#define PP_LSQ_PIPE 0
-#endif
-// PP_LSQ_QSMEM: q_i staged in shared memory once per projection (doubles the solve's smem)
+
 // PP_SLOT_TILED: the solver's working arrays (J/Q, R, b, Q^H b) in the slot-tiled layout
 #ifndef PP_SLOT_TILED
 #define PP_SLOT_TILED 1
@@ -460,9 +456,6 @@ struct RowsUnroll {
 #define PP_WORK(ptr, E) Tiled<R>{(ptr), static_cast<uint32_t>(E)}
 #else
 #define PP_WORK(ptr, E) Planar<R>{(ptr), a.S}
-#endif
-#ifndef PP_LSQ_QSMEM
-#define PP_LSQ_QSMEM 0
 #endif
 
 __device__ __forceinline__ void prefetch_line(const double* p) {
@@ -489,10 +482,9 @@ __device__ __forceinline__ void prefetch_column(const GA& Q, int col, int n, siz
 #endif
 }
 
-template <class R, class GA>
+template <class R, class GA, class CA, bool kUniform>
 __device__ bool lsq_solve_c(int n, double rank_tol, const GA& Q, const GA& Rm, const GA& B, const GA& Y,
-                            size_t s, const Planar<R>& C,
-                            size_t cs) {
+                            size_t s, const CA& C) {
   const cx<R> zero = czero<R>();
   R max_norm = rfrom<R>(0.0);
   for (int j = 0; j < n; ++j) {
@@ -504,9 +496,12 @@ PP_UNROLL_ROWS
   }
   const R tol = rmul(max_norm, rfrom<R>(rank_tol));
 
+  // kUniform (warp-collective column storage): a rank-deficient lane does not leave early; it
+  // finishes the solve on its own scratch with the result discarded, so the warp stays converged
+  bool ok = true;
   for (int k = 0; k < n; ++k) {
 PP_UNROLL_ROWS
-    for (int r = 0; r < n; ++r) C.st(r, cs, Q.ld(k * n + r, s));
+    for (int r = 0; r < n; ++r) C.st(r, Q.ld(k * n + r, s));
     const int rk = k * (k + 1) / 2;
     for (int pass = 0; pass < 2; ++pass) {
       for (int i = 0; i < k; ++i) {
@@ -514,53 +509,28 @@ PP_UNROLL_ROWS
         const int nxt = i + 1 < k ? i + 1 : (pass == 0 ? 0 : k + 1);
         if (nxt < n) prefetch_column<R>(Q, nxt, n, s);
         cx<R> rik = zero;
-#if PP_LSQ_PIPE
-        cx<R> qn = Q.ld(i * n, s);
-        for (int r = 0; r < n; ++r) {
-          const cx<R> q = qn;
-          if (r + 1 < n) qn = Q.ld(i * n + r + 1, s);
-          rik = cadd(rik, cmul(cconj(q), C.ld(r, cs)));
-        }
-        const cx<R> prev = pass == 0 ? zero : Rm.ld(i + rk, s);
-        Rm.st(i + rk, s, cadd(prev, rik));
-        qn = Q.ld(i * n, s);
-        for (int r = 0; r < n; ++r) {
-          const cx<R> q = qn;
-          if (r + 1 < n) qn = Q.ld(i * n + r + 1, s);
-          C.st(r, cs, csub(C.ld(r, cs), cmul(rik, q)));
-        }
-#elif PP_LSQ_QSMEM
-        // stage q_i in shared memory (right after this thread's column): read once from L2/HBM
-        const Planar<R> QI{C.base + static_cast<size_t>(n) * 2 * level<R>::L * C.S, C.S};
 PP_UNROLL_ROWS
-        for (int r = 0; r < n; ++r) QI.st(r, cs, Q.ld(i * n + r, s));
-PP_UNROLL_ROWS
-        for (int r = 0; r < n; ++r) rik = cadd(rik, cmul(cconj(QI.ld(r, cs)), C.ld(r, cs)));
+        for (int r = 0; r < n; ++r) rik = cadd(rik, cmul(cconj(Q.ld(i * n + r, s)), C.ld(r)));
         const cx<R> prev = pass == 0 ? zero : Rm.ld(i + rk, s);
         Rm.st(i + rk, s, cadd(prev, rik));
 PP_UNROLL_ROWS
-        for (int r = 0; r < n; ++r) C.st(r, cs, csub(C.ld(r, cs), cmul(rik, QI.ld(r, cs))));
-#else
-PP_UNROLL_ROWS
-        for (int r = 0; r < n; ++r) rik = cadd(rik, cmul(cconj(Q.ld(i * n + r, s)), C.ld(r, cs)));
-        const cx<R> prev = pass == 0 ? zero : Rm.ld(i + rk, s);
-        Rm.st(i + rk, s, cadd(prev, rik));
-PP_UNROLL_ROWS
-        for (int r = 0; r < n; ++r) C.st(r, cs, csub(C.ld(r, cs), cmul(rik, Q.ld(i * n + r, s))));
-#endif
+        for (int r = 0; r < n; ++r) C.st(r, csub(C.ld(r), cmul(rik, Q.ld(i * n + r, s))));
       }
     }
     R acc = rfrom<R>(0.0);
 PP_UNROLL_ROWS
-    for (int r = 0; r < n; ++r) acc = radd(acc, cabs2(C.ld(r, cs)));
+    for (int r = 0; r < n; ++r) acc = radd(acc, cabs2(C.ld(r)));
     const R rkk = rsqrt(acc);
-    if (rcmp(rkk, tol) <= 0) return false;
+    if (rcmp(rkk, tol) <= 0) {
+      if (!kUniform) return false;
+      ok = false;
+    }
     Rm.st(k + rk, s, cx<R>{rkk, rfrom<R>(0.0)});
     const R rinv = rdiv(rfrom<R>(1.0), rkk);
     cx<R> y = zero;
 PP_UNROLL_ROWS
     for (int r = 0; r < n; ++r) {
-      const cx<R> q = cmulr(C.ld(r, cs), rinv);
+      const cx<R> q = cmulr(C.ld(r), rinv);
       Q.st(k * n + r, s, q);
       y = cadd(y, cmul(cconj(q), B.ld(r, s)));  // y_k = <q_k, b> (linalg.hpp:117)
     }
@@ -569,10 +539,10 @@ PP_UNROLL_ROWS
   // back substitution R x = y (linalg.hpp:118-122); x_j overwrites C_j
   for (int j = n - 1; j >= 0; --j) {
     cx<R> acc = Y.ld(j, s);
-    for (int i = j + 1; i < n; ++i) acc = csub(acc, cmul(Rm.ld(j + i * (i + 1) / 2, s), C.ld(i, cs)));
-    C.st(j, cs, cdiv(acc, Rm.ld(j + j * (j + 1) / 2, s)));
+    for (int i = j + 1; i < n; ++i) acc = csub(acc, cmul(Rm.ld(j + i * (i + 1) / 2, s), C.ld(i)));
+    C.st(j, cdiv(acc, Rm.ld(j + j * (j + 1) / 2, s)));
   }
-  return true;
+  return ok;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -596,34 +566,87 @@ struct SlotInts {
 // ---------------------------------------------------------------------------------------------
 // trip kernel 2 (thread per path): least-squares Newton update for corrector / refinement slots
 // ---------------------------------------------------------------------------------------------
-template <class R>
-__global__ void __launch_bounds__(128, PP_LSQ_MINB) lsq_trip(const TrackArgs a) {
+// TMEM helpers: a CTA of four warps allocates `cols` columns of tensor memory (one warp allocates
+// and relinquishes its permit; fences around the barrier), and frees them at the end
+template <uint32_t kCols>
+__device__ __forceinline__ uint32_t tmem_alloc_cta(uint32_t* holder) {
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(holder))),
+                 "n"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  return *holder;
+}
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_free_cta(uint32_t base) {
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(base), "n"(kCols));
+}
+
+// kTmem: the column being orthogonalised lives in the thread's TMEM lane instead of shared
+// memory, which leaves the whole L1 to the Q columns (the axpy re-reads q_i right after the dot
+// product).  Its accesses are warp-collective, so a warp runs the solve if any lane needs it.
+template <class R, bool kTmem, int kThreads, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) lsq_trip(const TrackArgs a) {
   constexpr int L = level<R>::L;
   extern __shared__ double smem[];
   const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (s >= a.n_active) return;
+  const bool in_range = s < a.n_active;
   const SlotInts si{a.si, a.S};
-  const int mode = si(F_MODE, s);
-  if (mode != M_NEWTON && mode != M_REFINE) return;
+  const int mode = in_range ? si(F_MODE, s) : M_DONE;
+  const bool need = mode == M_NEWTON || mode == M_REFINE;
   const int n = a.plan.n;
   const Planar<R> X{a.x, a.S};
   const auto J = PP_WORK(a.J, n * n), Rm = PP_WORK(a.Rm, n * (n + 1) / 2), B = PP_WORK(a.B, n), Y = PP_WORK(a.Y, n);
-  const Planar<R> C{smem, blockDim.x};
-  const size_t cs = threadIdx.x;
-  const bool ok = lsq_solve_c<R>(n, a.rank_tol, J, Rm, B, Y, s, C, cs);
-  si(F_OK, s) = ok ? 1 : 0;
-  if (!ok) return;
-  // x += dx; update and iterate norms (tracker.cpp:258-264)
-  double dxn = 0.0, xn = 0.0;
-  for (int v = 0; v < n; ++v) {
-    const cx<R> dv = C.ld(v, cs);
-    const cx<R> xv = cadd(X.ld(v, s), dv);
-    X.st(v, s, xv);
-    dxn = f_max(dxn, cabsd(dv));
-    xn = f_max(xn, cabsd(xv));
+  if (!kTmem) {
+    if (!need) return;
+    const SmemRow<R> C{Planar<R>{smem, blockDim.x}, threadIdx.x};
+    const bool ok = lsq_solve_c<R, decltype(J), SmemRow<R>, false>(n, a.rank_tol, J, Rm, B, Y, s, C);
+    si(F_OK, s) = ok ? 1 : 0;
+    if (!ok) return;
+    // x += dx; update and iterate norms (tracker.cpp:258-264)
+    double dxn = 0.0, xn = 0.0;
+    for (int v = 0; v < n; ++v) {
+      const cx<R> dv = C.ld(v);
+      const cx<R> xv = cadd(X.ld(v, s), dv);
+      X.st(v, s, xv);
+      dxn = f_max(dxn, cabsd(dv));
+      xn = f_max(xn, cabsd(xv));
+    }
+    a.sd[D_DXN * a.S + s] = dxn;
+    a.sd[D_XN * a.S + s] = xn;
+  } else {
+    __shared__ uint32_t tmem_holder;
+    constexpr uint32_t kCols = kThreads == 256 ? 256 : 128;  // two warps per lane quarter at 256 threads
+    const uint32_t base = tmem_alloc_cta<kCols>(&tmem_holder);
+    const int warp = threadIdx.x >> 5;
+    const TmemRow<R> C{base + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + static_cast<uint32_t>((warp >> 2) * n * 4 * L)};
+    if (__any_sync(0xffffffffu, need)) {
+      const bool ok = lsq_solve_c<R, decltype(J), TmemRow<R>, true>(n, a.rank_tol, J, Rm, B, Y, s, C);
+      if (need) si(F_OK, s) = ok ? 1 : 0;
+      double dxn = 0.0, xn = 0.0;
+      for (int v = 0; v < n; ++v) {
+        const cx<R> dv = C.ld(v);  // warp-collective
+        if (need && ok) {
+          const cx<R> xv = cadd(X.ld(v, s), dv);
+          X.st(v, s, xv);
+          dxn = f_max(dxn, cabsd(dv));
+          xn = f_max(xn, cabsd(xv));
+        }
+      }
+      if (need && ok) {
+        a.sd[D_DXN * a.S + s] = dxn;
+        a.sd[D_XN * a.S + s] = xn;
+      }
+    }
+    tmem_free_cta<kCols>(base);
   }
-  a.sd[D_DXN * a.S + s] = dxn;
-  a.sd[D_XN * a.S + s] = xn;
   (void)L;
 }
 
@@ -1301,7 +1324,7 @@ __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
   if (s >= a.batch) return;
   const Planar<R> Q{a.a, a.batch}, Rm{a.r, a.batch}, B{a.b, a.batch}, Y{a.y, a.batch}, X{a.x, a.batch};
   const Planar<R> C{smem, blockDim.x};
-  const bool ok = lsq_solve_c<R>(a.n, a.rank_tol, Q, Rm, B, Y, s, C, threadIdx.x);
+  const bool ok = lsq_solve_c<R, Planar<R>, SmemRow<R>, false>(a.n, a.rank_tol, Q, Rm, B, Y, s, SmemRow<R>{C, threadIdx.x});
   a.ok[s] = ok ? 1 : 0;
   for (int v = 0; v < a.n; ++v) X.st(v, s, ok ? C.ld(v, threadIdx.x) : czero<R>());
 }
@@ -1313,11 +1336,12 @@ __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
 // monomial (the length of the Speelpenning prefix stack)
 #define PP_VARIANT(R, KM)                                                             \
   {KM, reinterpret_cast<const void*>(&pp::dev::ctrl_eval_trip<R, KM, false, PP_EVAL_MINB>),                     \
-   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R>),                              \
+   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, false, 128, PP_LSQ_MINB>),                              \
    reinterpret_cast<const void*>(&pp::dev::step_trip<R>),                             \
    reinterpret_cast<const void*>(&pp::dev::eval_kernel<R, KM>),                       \
    reinterpret_cast<const void*>(&pp::dev::lsq_kernel<R>),                            \
    reinterpret_cast<const void*>(&pp::dev::eval_coop<R, KM>),                         \
    reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, false>),                       \
    reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, true>),                        \
-   reinterpret_cast<const void*>(&pp::dev::ctrl_eval_trip<R, KM, true, (sizeof(R) < 32 ? 4 : 1)>)}
+   reinterpret_cast<const void*>(&pp::dev::ctrl_eval_trip<R, KM, true, (sizeof(R) < 32 ? 4 : 1)>),             \
+   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, true, 256, 2>)}

@@ -109,13 +109,16 @@ def test_track_bitwise(pp, name, system):
 def test_track_bitwise_modes(pp, monkeypatch, name, system, mode):
     """every engine gives the reference records: every trip in tail mode (a warp per path:
     eval_coop / lsq_coop), or never (a thread per path; small runs otherwise start in tail mode),
-    also with the open Jacobian row in tensor memory (PP200_TMEM)"""
+    also with the open Jacobian row and the Gram-Schmidt column in tensor memory"""
     if mode == "warp_per_path":
         monkeypatch.setenv("PP200_FORCE_COOP", "1")
     else:
         monkeypatch.setenv("PP200_TAIL_SLOTS", "0")
     if mode.endswith("tmem"):
         monkeypatch.setenv("PP200_TMEM", "1")
+        monkeypatch.setenv("PP200_LSQ_TMEM", "1")
+    else:
+        monkeypatch.setenv("PP200_TMEM", "0")
     test_track_bitwise(pp, name, system)
 
 
