@@ -508,7 +508,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     // launched slots are busy (PP200_COMPACT=0 disables it)
     const bool compact = env_size("PP200_COMPACT", 1) != 0;
     // compact when at most this fraction of the launched slots is busy (PP200_COMPACT_PCT)
-    const double compact_frac = static_cast<double>(std::min<size_t>(99, env_size("PP200_COMPACT_PCT", 90))) / 100.0;
+    const double compact_frac = static_cast<double>(std::min<size_t>(99, env_size("PP200_COMPACT_PCT", 95))) / 100.0;
     unsigned* holes = nullptr;
     if (compact) check(cudaMallocAsync(reinterpret_cast<void**>(&holes), (2 * S + 2) * sizeof(unsigned), stream), "alloc");
     auto maybe_compact = [&](unsigned long long nbusy, unsigned long long started) -> bool {
