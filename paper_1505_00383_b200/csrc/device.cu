@@ -303,8 +303,19 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   // the open Jacobian row in tensor memory (n*4L 32-bit columns per thread, at most 128; a CTA of
   // four warps covers the four TMEM lane quarters, four CTAs use all 512 columns); PP200_TMEM=0
   // keeps it in shared memory
-  const bool tmem = env_size("PP200_TMEM", 1) != 0 && static_cast<size_t>(n) * 4 * L <= 128 && eblock == 128 &&
+  bool tmem = env_size("PP200_TMEM", 1) != 0 && static_cast<size_t>(n) * 4 * L <= 128 && eblock == 128 &&
                     !dev::kEvalJGlobal;
+  uint32_t tmem_cols = 32;
+  while (tmem_cols < static_cast<uint32_t>(n) * 4 * L) tmem_cols *= 2;
+  if (tmem) {
+    // every resident CTA must get its columns at once (512 per SM), or tcgen05.alloc would stall
+    int per_sm = 0;
+    check(cudaFuncSetAttribute(var->ctrl_eval_tmem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(eblock * per_thread_smem / 2)), "cudaFuncSetAttribute");
+    check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var->ctrl_eval_tmem, eblock, eblock * per_thread_smem / 2),
+          "occupancy");
+    tmem = static_cast<uint32_t>(per_sm) * tmem_cols <= 512;
+  }
   const void* ctrl_eval_fn = tmem ? var->ctrl_eval_tmem : var->ctrl_eval_trip;
   const size_t eval_smem = static_cast<size_t>(eblock) * per_thread_smem / ((dev::kEvalJGlobal || tmem) ? 2 : 1);
   // least squares: the column being orthogonalised in shared memory, or (PP200_LSQ_TMEM=1, n*4L <= 128)
@@ -322,8 +333,9 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
         "cudaFuncSetAttribute");
   check(cudaFuncSetAttribute(lsq_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsq_smem)),
         "cudaFuncSetAttribute");
-  // slots: PP200_SLOTS_PER_SM (default 512) per SM, never more than the paths (whole blocks)
-  const size_t per_sm = std::max<size_t>(tblock, env_size("PP200_SLOTS_PER_SM", 512));
+  // slots: PP200_SLOTS_PER_SM per SM (default 512; 1024 in complex double, whose kernels are
+  // memory-latency bound and want more warps), never more than the paths (whole blocks)
+  const size_t per_sm = std::max<size_t>(tblock, env_size("PP200_SLOTS_PER_SM", L == 1 ? 1024 : 512));
   uint64_t blocks = (per_sm / tblock) * static_cast<uint64_t>(prop.multiProcessorCount);
   blocks = std::min<uint64_t>(blocks, (count + tblock - 1) / tblock);
   blocks = std::max<uint64_t>(blocks, 1);
@@ -443,6 +455,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   unsigned long long* mbox = nullptr;
   check(cudaMallocHost(&mbox, 2 * sizeof(unsigned long long)), "cudaMallocHost");
   a.n_active = S;
+  a.tmem_cols = tmem_cols;
   {
     const dim3 blk(tblock);
     dim3 grid(static_cast<unsigned>(blocks));

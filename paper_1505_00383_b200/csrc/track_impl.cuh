@@ -1,25 +1,27 @@
 // track_impl.cuh -- sm_100a kernels of the many-path tracker.
 //
-// Design: one CUDA thread owns one path slot for the whole launch (persistent
-// grid, one wave).  A slot runs the reference's per-path state machine -- predict, up to
-// max_newton corrector iterations, step control, status, finalize -- and refills itself from a
-// global atomic start counter when its path ends, so paths that finish or diverge release their
-// thread immediately (the reference's compaction, tracker.cpp:340-387, without a host round trip).
-// Every loop trip performs exactly one "heavy" operation per slot -- an evaluation of H and
-// dH/dx at the slot's point followed (in corrector/refinement modes) by a least-squares solve --
-// so all lanes of a warp execute the expensive code together even though each lane is at a
-// different place on a different path; only the cheap bookkeeping between trips diverges.
+// Design: one CUDA thread owns one path slot.  A slot runs the reference's
+// per-path state machine -- predict, up to max_newton corrector iterations, step control,
+// status, finalize -- and refills itself from a global atomic start counter when its path ends,
+// so paths that finish or diverge release their thread immediately (the reference's compaction,
+// tracker.cpp:340-387, without a host round trip).  Every trip performs exactly one "heavy"
+// operation per slot -- an evaluation of H and dH/dx at the slot's point followed (in corrector /
+// refinement modes) by a least-squares solve -- so all lanes of a warp execute the expensive code
+// together even though each lane is at a different place on a different path; only the cheap
+// bookkeeping diverges.  A trip is two kernels (ctrl_eval_trip, lsq_trip); when few paths
+// remain, tail mode gives each path a whole warp (step_trip, eval_coop, lsq_coop).
 //
 // Per-path results are bitwise identical to the reference CPU tracker: every floating-point
 // operation is the reference's (xprec.cuh), executed in the reference's order per path, and the
 // reference's per-path results do not depend on batching (test_tracker.cpp:383-432).
 //
-// Memory: the working point x and the open Jacobian row live in shared memory (dynamic indices
-// from the instruction tables); the Jacobian / Q, R, right-hand side, history and accepted point
-// live in global memory in a slot-minor planar layout (element e, limb-plane p, slot s at
-// ((e*P)+p)*S+s) so a warp's 32 slots touch 32 consecutive doubles -- the paper's transposed
-// layout (Table 5/7).  The Gram-Schmidt column being orthogonalised and the Speelpenning
-// prefix stack is a dynamically indexed local array (KMAX).
+// Memory: the working point x is in shared memory and the open Jacobian row in tensor memory
+// (or shared memory), both indexed by the instruction tables; the Gram-Schmidt column being
+// orthogonalised is in shared memory; slot state, history and the accepted point are global,
+// slot-minor planar (element e, limb-plane p, slot s at ((e*P)+p)*S+s: a warp's 32 slots touch
+// 32 consecutive doubles, the paper's transposed layout, Table 5/7); the solver's
+// working arrays (Jacobian / Q, R, b, Q^H b) are slot-tiled (Tiled<R>).  The Speelpenning prefix
+// stack is a dynamically indexed local array (KMAX).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -57,14 +59,6 @@ struct Planar {
   static constexpr int L = level<R>::L;
   double* base;
   size_t S;  // stride between planes (slots, or blockDim for shared memory)
-
-  // an opaque copy: addresses derived from it cannot be hoisted above this point (used at the
-  // top of long loops so loop-invariant per-plane addresses do not pin registers)
-  __device__ __forceinline__ Planar fresh() const {
-    Planar q = *this;
-    asm volatile("" : "+l"(q.base), "+l"(q.S));
-    return q;
-  }
 
   // Offsets are formed in 32 bits (one IMAD per element instead of 64-bit multiplies per plane);
   // device_track checks that every planar array holds fewer than 2^32 doubles.
@@ -979,12 +973,12 @@ __global__ void __launch_bounds__(128, kMinBlocks) ctrl_eval_trip(const TrackArg
   // TMEM variant: the CTA's open rows live in tensor memory (warp w: lanes 32*(w%4) .. +31,
   // columns (w/4) * n*4L ..); one warp allocates, all fence around the barrier
   __shared__ uint32_t tmem_base;
-  constexpr uint32_t kCols = kTmem ? 128u : 0u;
+  const uint32_t kCols = a.tmem_cols;  // power of two >= n*4L, chosen by the host
   if (kTmem) {
     if (threadIdx.x < 32) {
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                        static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base))),
-                   "n"(kCols));
+                   "r"(kCols));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -1046,7 +1040,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) ctrl_eval_trip(const TrackArg
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     if (threadIdx.x < 32)
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "n"(kCols));
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(kCols));
   }
 }
 
