@@ -529,6 +529,18 @@ def track_all(h: Homotopy, starts: Starts, cfg: TrackConfig | None = None, lo: i
     return rec.solution_set(stats)
 
 
+def compact_scan(status) -> dict:
+    """compact_scan (tracker.hpp:46-54, tracker.cpp:51-65): inclusive prefix scan over
+    [status == active], 1-based job labels of the active slots and their slot indices -- the
+    paper's compaction step (Table 3).  The device does the same per trip without a
+    host round trip (slot refill and tail compaction)."""
+    active = (np.asarray(status, dtype=np.int8) == ACTIVE).astype(np.uint32)
+    scan = np.cumsum(active, dtype=np.uint32)
+    path_idx = np.flatnonzero(active).astype(np.uint32)
+    return {"scan": scan, "active_count": int(scan[-1]) if len(scan) else 0,
+            "job_idx": np.arange(1, len(path_idx) + 1, dtype=np.uint32), "path_idx": path_idx}
+
+
 def eval_batch(h: Homotopy, points: np.ndarray, t: np.ndarray, device: int = 0):
     """eval_system_batch (evaldiff.hpp:228-230) on the device: points [B][dim][2L], t [B][L] ->
     (sys [B][n_polys][2L], jac [B][n_polys*dim][2L])."""

@@ -221,3 +221,12 @@ def test_warp_accumulation_lists(pp, system):
             want = [ts[i] + 1 + j for i in range(nt) if ti[i, 0] == p
                     for j in range(ti[i, 1]) if (pos[ti[i, 2] + j] & 0xFFFF) == v]
         assert list(lst) == want
+
+
+def test_compact_scan_known_answer(pp):
+    """test_tracker.cpp:62-78 / acceptance.cpp:91-102: (0,1,0,-1,0) -> scan (1,1,2,2,3),
+    job (1,2,3), path (0,2,4)"""
+    r = pp.compact_scan([0, 1, 0, -1, 0])
+    assert list(r["scan"]) == [1, 1, 2, 2, 3] and r["active_count"] == 3
+    assert list(r["job_idx"]) == [1, 2, 3] and list(r["path_idx"]) == [0, 2, 4]
+    assert pp.compact_scan([])["active_count"] == 0
