@@ -177,23 +177,16 @@ __device__ __forceinline__ cx<R> ld_flat(const double* p) {
   return z;
 }
 
-// ---------------------------------------------------------------------------------------------
-// evaluation of H(x, t) and dH/dx (reference evaldiff.cpp:259-374, fused per term)
-// ---------------------------------------------------------------------------------------------
-// X: the point (shared memory, this thread's column); JR: open Jacobian row accumulator (shared);
-// outputs: B[p] = -H_p (the least-squares right-hand side, tracker.cpp:249), J[v*n_polys + p];
-// resid_d = max_p to_double(|H_p|) (tracker.cpp:247-251), resid_r = max_p |H_p| at level R
-// (tracker.cpp:488-494).  The coefficient, monomial and sum stages of the reference are fused: the
-// value/derivative slots of one term are produced in registers and accumulated immediately.
-// Because the plan is polynomial-major (evaldiff.cpp:200-236), only one row of H/J is open.
 // One term of the plan at the point X (this thread's column xs): the coefficient, monomial and
 // sum-stage products of evaldiff.cpp:259-374 for term i.  sys_add(v) receives the term's
 // contribution to H_poly (c, or c * value), jac_add(j, var, w) the contribution of its j-th
-// variable to dH_poly/dx_var, in the reference's order.  The Speelpenning prefix stack is a
+// variable to dH_poly/dx_var, in the reference's order; jac_pre(var) is called before w is
+// computed.  The Speelpenning prefix stack is a
 // dynamically indexed array (local memory, L1-resident), so the code stays compact for any KMAX.
-template <class R, int KMAX, class SysF, class JacF>
+template <class R, int KMAX, class SysF, class JacF, class PreF>
 __device__ __forceinline__ void eval_term(const PlanArgs& pa, int i, const Planar<R>& X, size_t xs, const R& t,
-                                          const R& u, int& poly_out, SysF&& sys_add, JacF&& jac_add) {
+                                          const R& u, int& poly_out, SysF&& sys_add, JacF&& jac_add,
+                                          PreF&& jac_pre) {
   constexpr int L = level<R>::L;
   const int4 ti = __ldg(reinterpret_cast<const int4*>(pa.term_info) + i);
   const int k = ti.y, po = ti.z, nb = ti.w & 0xff, bo = ti.w >> 8;
@@ -238,6 +231,7 @@ __device__ __forceinline__ void eval_term(const PlanArgs& pa, int i, const Plana
   // derivative contribution w = c*d (scaled by the exponent when e != 1) of variable j
   auto contribute = [&](int j, cx<R> d) {
     const uint32_t pe = __ldg(pv + j);
+    jac_pre(static_cast<int>(pe & 0xffffu));  // lets the accumulator fetch its old value early
     if (nb > 0) d = cmul(d, aux);
     cx<R> w = cmul(c, d);
     const uint32_t e = pe >> 16;
@@ -286,6 +280,10 @@ struct SmemRow {
   size_t ls;
   __device__ __forceinline__ cx<R> ld(int v) const { return P.ld(v, ls); }
   __device__ __forceinline__ void st(int v, const cx<R>& z) const { P.st(v, ls, z); }
+  struct Pending {};
+  __device__ __forceinline__ void issue(int, Pending&) const {}
+  __device__ __forceinline__ void finish_add(int v, Pending&, const cx<R>& w) const { st(v, cadd(ld(v), w)); }
+  __device__ __forceinline__ void drain() const {}
 };
 
 template <int W>
@@ -328,6 +326,53 @@ struct TmemIO<16> {
   }
 };
 
+// asynchronous forms: the load's registers become valid at tmem_wait_ld (which takes them as
+// operands, so the compiler cannot use them earlier); stores complete at tmem_wait_st
+template <int W>
+__device__ __forceinline__ void tmem_ld_issue(uint32_t a, uint32_t (&r)[W]) {
+  if constexpr (W == 4) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(a) : "memory");
+  } else {
+#pragma unroll
+    for (int q = 0; q < W / 8; ++q)
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(r[8 * q]), "=r"(r[8 * q + 1]), "=r"(r[8 * q + 2]), "=r"(r[8 * q + 3]), "=r"(r[8 * q + 4]),
+                     "=r"(r[8 * q + 5]), "=r"(r[8 * q + 6]), "=r"(r[8 * q + 7])
+                   : "r"(a + 8 * q) : "memory");
+  }
+}
+template <int W>
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[W]) {
+  if constexpr (W == 4) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3])::"memory");
+  } else {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7])::"memory");
+#pragma unroll
+    for (int q = 1; q < W / 8; ++q)
+      asm volatile(""
+                   : "+r"(r[8 * q]), "+r"(r[8 * q + 1]), "+r"(r[8 * q + 2]), "+r"(r[8 * q + 3]), "+r"(r[8 * q + 4]),
+                     "+r"(r[8 * q + 5]), "+r"(r[8 * q + 6]), "+r"(r[8 * q + 7])::"memory");
+  }
+}
+template <int W>
+__device__ __forceinline__ void tmem_st_issue(uint32_t a, const uint32_t (&r)[W]) {
+  if constexpr (W == 4) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(r[0]), "r"(r[1]), "r"(r[2]),
+                 "r"(r[3])
+                 : "memory");
+  } else {
+#pragma unroll
+    for (int q = 0; q < W / 8; ++q)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(a + 8 * q),
+                   "r"(r[8 * q]), "r"(r[8 * q + 1]), "r"(r[8 * q + 2]), "r"(r[8 * q + 3]), "r"(r[8 * q + 4]),
+                   "r"(r[8 * q + 5]), "r"(r[8 * q + 6]), "r"(r[8 * q + 7])
+                   : "memory");
+  }
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 template <class R>
 struct TmemRow {
   static constexpr int L = level<R>::L, W = 4 * level<R>::L;  // 32-bit columns per complex value
@@ -335,6 +380,7 @@ struct TmemRow {
   __device__ __forceinline__ cx<R> ld(int v) const {
     uint32_t r[W];
     __syncwarp();
+    tmem_wait_st();  // an earlier asynchronous store (finish_add) may still be in flight
     TmemIO<W>::ld(base + static_cast<uint32_t>(v) * W, r);
     cx<R> z;
 #pragma unroll
@@ -346,6 +392,11 @@ struct TmemRow {
   }
   __device__ __forceinline__ void st(int v, const cx<R>& z) const {
     uint32_t r[W];
+    pack(z, r);
+    __syncwarp();
+    TmemIO<W>::st(base + static_cast<uint32_t>(v) * W, r);
+  }
+  static __device__ __forceinline__ void pack(const cx<R>& z, uint32_t (&r)[W]) {
 #pragma unroll
     for (int l = 0; l < L; ++l) {
       const double a = level<R>::get(z.re, l), b = level<R>::get(z.im, l);
@@ -354,8 +405,36 @@ struct TmemRow {
       r[2 * (L + l)] = static_cast<uint32_t>(__double2loint(b));
       r[2 * (L + l) + 1] = static_cast<uint32_t>(__double2hiint(b));
     }
+  }
+  static __device__ __forceinline__ cx<R> unpack(const uint32_t (&r)[W]) {
+    cx<R> z;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      level<R>::set(z.re, l, __hiloint2double(static_cast<int>(r[2 * l + 1]), static_cast<int>(r[2 * l])));
+      level<R>::set(z.im, l, __hiloint2double(static_cast<int>(r[2 * (L + l) + 1]), static_cast<int>(r[2 * (L + l)])));
+    }
+    return z;
+  }
+  // read-modify-write of one entry with the load issued early: issue() before the contribution
+  // is computed, finish_add() after; the store completes at the next issue() (or drain())
+  struct Pending {
+    uint32_t r[W];
+  };
+  __device__ __forceinline__ void issue(int v, Pending& p) const {
     __syncwarp();
-    TmemIO<W>::st(base + static_cast<uint32_t>(v) * W, r);
+    tmem_wait_st();
+    tmem_ld_issue<W>(base + static_cast<uint32_t>(v) * W, p.r);
+  }
+  __device__ __forceinline__ void finish_add(int v, Pending& p, const cx<R>& w) const {
+    __syncwarp();
+    tmem_wait_ld<W>(p.r);
+    uint32_t r[W];
+    pack(cadd(unpack(p.r), w), r);
+    tmem_st_issue<W>(base + static_cast<uint32_t>(v) * W, r);
+  }
+  __device__ __forceinline__ void drain() const {
+    __syncwarp();
+    tmem_wait_st();
   }
 };
 
@@ -405,15 +484,18 @@ __device__ void eval_hj(const PlanArgs& pa, const Planar<R>& X, const ROW& JR, s
     const int poly = __ldg(pa.term_info + 4 * i);
     while (cur < poly) flush(cur++);
     int p_unused;
+    typename ROW::Pending pend;
     eval_term<R, KMAX>(
         pa, i, X, ls, t, u, p_unused, [&](const cx<R>& v) { sacc = cadd(sacc, v); },
 #if PP_EVAL_JGLOBAL
-        [&](int, int var, const cx<R>& w) { J.st(var * np + poly, gs, cadd(J.ld(var * np + poly, gs), w)); });
+        [&](int, int var, const cx<R>& w) { J.st(var * np + poly, gs, cadd(J.ld(var * np + poly, gs), w)); },
+        [&](int) {});
 #else
-        [&](int, int var, const cx<R>& w) { JR.st(var, cadd(JR.ld(var), w)); });
+        [&](int, int var, const cx<R>& w) { JR.finish_add(var, pend, w); }, [&](int var) { JR.issue(var, pend); });
 #endif
   }
   while (cur < np) flush(cur++);
+  JR.drain();
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1101,7 +1183,7 @@ __global__ void __launch_bounds__(128) eval_coop(const TrackArgs a) {
     int poly;
     eval_term<R, KMAX>(
         pa, i, XS, 0, t, u, poly, [&](const cx<R>& v) { SL.st(slot, 0, v); },
-        [&](int j, int, const cx<R>& w) { SL.st(slot + 1 + j, 0, w); });
+        [&](int j, int, const cx<R>& w) { SL.st(slot + 1 + j, 0, w); }, [&](int) {});
   }
   __syncwarp();
   double resid = 0.0;
