@@ -418,6 +418,22 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
 
   cudaStream_t stream;
   check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
+  // PP200_L2_PERSIST=1: mark the solver's Jacobian/Q array as L2-persisting for the fraction that
+  // fits the device's persisting-L2 limit (the rest streams), so part of the slots re-read their Q
+  // from L2 instead of HBM on every projection
+  const bool l2_persist = env_size("PP200_L2_PERSIST", 0) != 0;
+  if (l2_persist && prop.persistingL2CacheMaxSize > 0) {
+    const size_t jbytes = nJ * cw * S * sizeof(double);
+    check(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, prop.persistingL2CacheMaxSize), "L2 limit");
+    cudaStreamAttrValue attr{};
+    attr.accessPolicyWindow.base_ptr = a.J;
+    attr.accessPolicyWindow.num_bytes = std::min<size_t>(jbytes, prop.accessPolicyMaxWindowSize);
+    attr.accessPolicyWindow.hitRatio = std::min<float>(
+        1.0f, static_cast<float>(prop.persistingL2CacheMaxSize) / static_cast<float>(attr.accessPolicyWindow.num_bytes));
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    check(cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &attr), "access policy");
+  }
   cudaEvent_t e0, e1, e2, e3;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -599,6 +615,23 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
         for (size_t j = 0; j < graph_trips; ++j) launch_trip(busy + j, nullptr);
         launches -= (coop ? 3 : 2) * graph_trips;  // counted per graph launch below
         check(cudaStreamEndCapture(stream, &graph), "end capture");
+        if (l2_persist && prop.persistingL2CacheMaxSize > 0) {
+          // make sure every captured kernel carries the stream's L2 access policy
+          cudaStreamAttrValue sattr{};
+          check(cudaStreamGetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &sattr), "get attr");
+          size_t nn = 0;
+          check(cudaGraphGetNodes(graph, nullptr, &nn), "graph nodes");
+          std::vector<cudaGraphNode_t> nodes(nn);
+          check(cudaGraphGetNodes(graph, nodes.data(), &nn), "graph nodes");
+          for (cudaGraphNode_t nd : nodes) {
+            cudaGraphNodeType ty;
+            check(cudaGraphNodeGetType(nd, &ty), "node type");
+            if (ty != cudaGraphNodeTypeKernel) continue;
+            cudaKernelNodeAttrValue kv{};
+            kv.accessPolicyWindow = sattr.accessPolicyWindow;
+            check(cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributeAccessPolicyWindow, &kv), "node attr");
+          }
+        }
         check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
       };
       capture();
@@ -649,6 +682,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   if (exec) cudaGraphExecDestroy(exec);
   if (graph) cudaGraphDestroy(graph);
   cudaFreeHost(mbox);
+  if (l2_persist && prop.persistingL2CacheMaxSize > 0) cudaCtxResetPersistingL2Cache();
   cudaStreamDestroy(stream);
 
   // terminal divergence classification: m_est = log(growth) / log(shrink) with the host libm
