@@ -17,6 +17,7 @@
 #include <cstdint>
 
 #if defined(__CUDACC__)
+#define PP_UNROLL _Pragma("unroll")
 #define PP_HD __host__ __device__ __forceinline__
 // quad-double operations are 100-250 binary64 instructions each; they are real calls on the
 // device so that kernels built from them stay compact (code size, compile time, I-cache)
@@ -24,6 +25,7 @@
 #else
 #define PP_HD inline
 #define PP_QD_FN inline
+#define PP_UNROLL
 #endif
 
 // host-only operation counter for the work model (scripts/count_ops.cpp defines PP_COUNT_OPS)
@@ -341,7 +343,7 @@ PP_QD_FN qd_t radd(qd_t a, qd_t b) {
   int k = 0;
   // the six remaining limbs: while fewer than four outputs exist they feed the accumulator,
   // afterwards they fold into the fifth channel (the reference's tail loop, after x4 = u + v)
-#pragma unroll
+PP_UNROLL
   for (int step = 0; step < 6; ++step) {
     double t = qdi::take(qa, qb);
     if (k < 4) {
@@ -483,7 +485,7 @@ PP_QD_FN qd_t rsqrt(qd_t a) {
   if (a.c0 == 0.0 && a.c1 == 0.0 && a.c2 == 0.0 && a.c3 == 0.0) return qd_make(0.0);
   qd_t r = qd_make(f_div(1.0, f_sqrt(a.c0)));
   qd_t h{f_mul(a.c0, 0.5), f_mul(a.c1, 0.5), f_mul(a.c2, 0.5), f_mul(a.c3, 0.5)};
-#pragma unroll
+PP_UNROLL
   for (int it = 0; it < 3; ++it) {
     // r += (0.5 - h*(r*r)) * r, with double - QD == (-QD) + double (xprec.hpp:392)
     qd_t corr = radd(rneg(rmul(h, rmul(r, r))), 0.5);
