@@ -5,13 +5,13 @@ import sys
 import threading
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_1505_00383_b200 as P  # noqa: E402
 
 paths = int(os.environ.get("PATHS", "262144"))
 offset = int(os.environ.get("OFFSET", "1000000"))
 K = int(os.environ.get("K", "2"))
-root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+root = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 f = P.parse_system(open(os.path.join(root, "tests", "data", "cyclic10.sys")).read())
 g, st = P.total_degree_start(f, "dd")
 h = P.make_homotopy(f, g, P.random_gamma(1), "dd")

@@ -2,11 +2,11 @@
 (oracle/_ref) on small configs, then a throughput probe.  Not part of the test suite."""
 import sys, time, os
 import numpy as np
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import oracle as O
 import paper_1505_00383_b200 as P
 
-DATA = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "data")
+DATA = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "..", "tests", "data")
 
 
 def compare(name, r, m):
