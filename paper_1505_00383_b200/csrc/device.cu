@@ -303,8 +303,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   // the open Jacobian row in tensor memory (n*4L 32-bit columns per thread, at most 128; a CTA of
   // four warps covers the four TMEM lane quarters, four CTAs use all 512 columns); PP200_TMEM=0
   // keeps it in shared memory
-  bool tmem = env_size("PP200_TMEM", 1) != 0 && static_cast<size_t>(n) * 4 * L <= 128 && eblock == 128 &&
-                    !dev::kEvalJGlobal;
+  bool tmem = env_size("PP200_TMEM", 1) != 0 && static_cast<size_t>(n) * 4 * L <= 128 && eblock == 128;
   uint32_t tmem_cols = 32;
   while (tmem_cols < static_cast<uint32_t>(n) * 4 * L) tmem_cols *= 2;
   if (tmem) {
@@ -317,7 +316,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     tmem = static_cast<uint32_t>(per_sm) * tmem_cols <= 512;
   }
   const void* ctrl_eval_fn = tmem ? var->ctrl_eval_tmem : var->ctrl_eval_trip;
-  const size_t eval_smem = static_cast<size_t>(eblock) * per_thread_smem / ((dev::kEvalJGlobal || tmem) ? 2 : 1);
+  const size_t eval_smem = static_cast<size_t>(eblock) * per_thread_smem / (tmem ? 2 : 1);
   // least squares: the column being orthogonalised in shared memory, or (PP200_LSQ_TMEM=1, n*4L <= 128)
   // in tensor memory with 256-thread CTAs, two per SM (256 TMEM columns each), leaving L1 to Q
   bool lsq_tm = env_size("PP200_LSQ_TMEM", 0) != 0 && static_cast<size_t>(n) * 4 * L <= 128 && tblock == 128;

@@ -13,11 +13,6 @@ namespace pp {
 namespace dev {
 
 constexpr int kHistDepth = 5;  // predictor history depth (reference tracker.cpp:87)
-#if defined(PP_EVAL_JGLOBAL) && PP_EVAL_JGLOBAL
-constexpr bool kEvalJGlobal = true;  // experiment: dH/dx accumulated in global memory
-#else
-constexpr bool kEvalJGlobal = false;
-#endif
 // slot-state field counts (enums F_*, R_*, D_* in track_impl.cuh)
 constexpr int kIntFields = 14, kRealFields = 4, kDblFields = 3;
 

@@ -29,12 +29,6 @@
 #include "kernels.hpp"
 #include "xprec.cuh"
 
-// PP_EVAL_JGLOBAL: the thread-per-path evaluation accumulates dH/dx in the global array instead
-// of an open row in shared memory (half the shared memory per thread)
-#ifndef PP_EVAL_JGLOBAL
-#define PP_EVAL_JGLOBAL 0
-#endif
-
 // register budgets of the trip kernels (minimum resident 128-thread blocks per SM)
 #ifndef PP_LSQ_MINB
 #define PP_LSQ_MINB 3
@@ -452,14 +446,7 @@ __device__ void eval_hj(const PlanArgs& pa, const Planar<R>& X, const ROW& JR, s
   const cx<R> zero = czero<R>();
   const R u = rsub(rfrom<R>(1.0), t);  // ws.set_t: 1 - t at level R (evaldiff.hpp:198-201)
 
-#if PP_EVAL_JGLOBAL
-  // the Jacobian accumulates in place in the global (tiled) array: zeroed first, then every
-  // contribution added in plan order -- the same additions as the open-row version
-  (void)JR;
-  for (int e = 0; e < n * np; ++e) J.st(e, gs, zero);
-#else
   for (int v = 0; v < n; ++v) JR.st(v, zero);
-#endif
   cx<R> sacc = zero;
   resid_d = 0.0;
   resid_r = rfrom<R>(0.0);
@@ -470,12 +457,10 @@ __device__ void eval_hj(const PlanArgs& pa, const Planar<R>& X, const ROW& JR, s
     R m = cabsr(sacc);
     resid_d = f_max(resid_d, rtod(m));
     if (rcmp(m, resid_r) > 0) resid_r = m;
-#if !PP_EVAL_JGLOBAL
     for (int v = 0; v < n; ++v) {
       J.st(v * np + p, gs, JR.ld(v));
       JR.st(v, zero);
     }
-#endif
     sacc = zero;
   };
 
@@ -487,12 +472,7 @@ __device__ void eval_hj(const PlanArgs& pa, const Planar<R>& X, const ROW& JR, s
     typename ROW::Pending pend;
     eval_term<R, KMAX>(
         pa, i, X, ls, t, u, p_unused, [&](const cx<R>& v) { sacc = cadd(sacc, v); },
-#if PP_EVAL_JGLOBAL
-        [&](int, int var, const cx<R>& w) { J.st(var * np + poly, gs, cadd(J.ld(var * np + poly, gs), w)); },
-        [&](int) {});
-#else
         [&](int, int var, const cx<R>& w) { JR.finish_add(var, pend, w); }, [&](int var) { JR.issue(var, pend); });
-#endif
   }
   while (cur < np) flush(cur++);
   JR.drain();
