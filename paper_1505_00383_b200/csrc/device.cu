@@ -482,9 +482,9 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     // lsq_coop), bitwise identical to the thread-per-path kernels
     const size_t el = static_cast<size_t>(2) * L * sizeof(double);  // bytes per complex value
     const size_t ecoop_warp = (static_cast<size_t>(n) + plan.n_slots()) * el;
-    // Q and R in shared memory while they take at most PP200_COOP_SMEM_KB (16) KB per warp, else
+    // Q and R in shared memory while they take at most PP200_COOP_SMEM_KB (4) KB per warp, else
     // left in the global arrays (more warps per SM)
-    const bool coop_global = static_cast<size_t>(n) * n * el > env_size("PP200_COOP_SMEM_KB", 16) * 1024;
+    const bool coop_global = static_cast<size_t>(n) * n * el > env_size("PP200_COOP_SMEM_KB", 4) * 1024;
     const void* lsq_coop_fn = coop_global ? var->lsq_coop_g : var->lsq_coop;
     const size_t lcoop_warp =
         (coop_global ? static_cast<size_t>(4) * n : static_cast<size_t>(n) * n + 4 * n + n * (n + 1) / 2) * el;
