@@ -4,11 +4,17 @@ double-double on 1..8 B200 (BASELINE.json metric), against the reference CPU tra
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--paths B]
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
 
-A step tracks B start paths of the 3,628,800-path total-degree start set to their terminal status
-(success / failed / diverged after finalize) on every GPU.  Each (step, rank) takes its own
-contiguous chunk of start indices, spread over the index space by a golden-ratio sequence, so N
-GPUs do N times the work (weak scaling) with no data-path collective; the only
-torch.distributed traffic is the barrier and the max-over-ranks timing.
+A step tracks B start paths per GPU of the 3,628,800-path total-degree start set to their terminal
+status (success / failed / diverged after finalize).  Step s takes a contiguous chunk of N*B start
+indices, spread over the index space by a golden-ratio sequence, and rank r tracks the block-cyclic
+shard r of it (blocks of 64 indices, pp_shard), so N GPUs do N times the work (weak scaling) with
+no data-path collective; the only torch.distributed traffic is the barrier and the
+max-over-ranks timing.  `--gpus N` without torchrun launches the N ranks itself (one per GPU;
+ranks share a GPU round-robin, over gloo, when the box has fewer).
+
+Before the timed steps every rank checks its GPU once at the bench's size: a full-occupancy call
+over the 262,144 paths of tests/golden/track_cyclic10_dd_prod.npz must reproduce the reference
+records of that file bit for bit, or the bench exits with an error instead of printing a number.
 
 value  = paths / device time of the tracking trips (CUDA events on the library's stream, inputs
          resident), max over ranks;
@@ -44,10 +50,27 @@ def chunk_offset(c: int, count: int, B: int) -> int:
     return int(math.floor(((c + 1) * PHI) % 1.0 * (count - B))) // 64 * 64
 
 
-def dist_setup():
+SHARD_BLOCK = 64
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: relaunch this script as N ranks on this node."""
+    import socket
+
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def dist_setup(cuda: bool = True):
     """One process per GPU (torchrun).  The data path has no collective; torch.distributed only
-    carries the barrier and the max-over-ranks timing.  PP200_DIST_BACKEND=gloo (with more ranks
-    than GPUs, ranks share devices round-robin) exercises the multi-rank logic on one GPU."""
+    carries the barrier and the max-over-ranks timing.  With more ranks than GPUs the ranks share
+    devices round-robin and use gloo (NCCL refuses two ranks on one device); PP200_DIST_BACKEND
+    overrides the choice."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -56,9 +79,12 @@ def dist_setup():
         import torch
         import torch.distributed as dist
 
-        local = local % max(1, torch.cuda.device_count())
-        torch.cuda.set_device(local)
-        dist.init_process_group(os.environ.get("PP200_DIST_BACKEND", "nccl"))
+        ndev = torch.cuda.device_count() if cuda else 0
+        backend = os.environ.get("PP200_DIST_BACKEND", "nccl" if ndev >= world else "gloo")
+        if ndev:
+            local = local % ndev
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
     return world, rank, local, dist
 
 
@@ -161,7 +187,7 @@ def cpu_reference_sample(text: str, lo: int, hi: int, threads: int, budget_s: fl
 
     if O.ref is None:
         raise RuntimeError("oracle/_ref/libppref.so (the reference build) is not present")
-    gam = complex(*_gamma_pair())
+    gam = O.ref_random_gamma(GAMMA_SEED)  # the reference's own random_gamma: no product code on this arm
     span = hi - lo
     done = [0] * threads
     t_end = time.perf_counter() + budget_s
@@ -184,13 +210,6 @@ def cpu_reference_sample(text: str, lo: int, hi: int, threads: int, budget_s: fl
     for t in ths:
         t.join()
     return sum(done), time.perf_counter() - t0, "reference"
-
-
-def _gamma_pair():
-    import paper_1505_00383_b200 as P
-
-    g = P.random_gamma(GAMMA_SEED)
-    return g.real, g.imag
 
 
 def run_reference_arm(args, world, rank):
@@ -235,6 +254,29 @@ def fp64_peak_ops(device: int) -> float | None:
         return None
 
 
+def validate_engine(P, h, starts, cfg, device):
+    """One full-occupancy call (262,144 cyclic-10 dd paths) whose records must equal the reference
+    records of tests/golden/track_cyclic10_dd_prod.npz bit for bit (8 ranges of 128 paths spread
+    over the call).  Raises SystemExit on any difference.  Returns the call's device seconds."""
+    gp = os.path.join(ROOT, "tests", "golden", "track_cyclic10_dd_prod.npz")
+    with np.load(gp) as z:
+        g = {k: z[k] for k in z.files}
+    lo, hi, per = int(g["call_lo"]), int(g["call_hi"]), int(g["range_len"])
+    sol = P.track_all(h, starts, cfg, lo=lo, hi=hi, device=device)
+    keys = ["path_id", "status", "reason", "steps", "newton_iters", "rejections", "x", "residual"]
+    for i, a in enumerate(g["range_lo"]):
+        off = int(a) - lo
+        for k in keys:
+            got = np.ascontiguousarray(getattr(sol, k)[off:off + per])
+            want = np.ascontiguousarray(g[k][i * per:(i + 1) * per])
+            if got.dtype == np.float64:
+                got, want = got.view(np.uint64), want.view(np.uint64)
+            if not np.array_equal(got, want):
+                raise SystemExit(f"bench self-check FAILED on device {device}: field {k} differs from the reference "
+                                 f"records in [{int(a)}, {int(a) + per})")
+    return sol.stats["device_ms"] / 1e3, len(g["range_lo"]) * per
+
+
 def run_ours(args, world, rank, local, dist):
     import paper_1505_00383_b200 as P
     from paper_1505_00383_b200 import work as W
@@ -252,13 +294,15 @@ def run_ours(args, world, rank, local, dist):
     info = h.info
 
     def step(s):
-        c = s * world + rank
-        lo = chunk_offset(c, count, B)
+        lo = chunk_offset(s, count, world * B)
+        shard = (rank, world, SHARD_BLOCK) if world > 1 else None
         t0 = time.perf_counter()
-        sol = P.track_all(h, starts, cfg, lo=lo, hi=lo + B, device=local, records=records)
+        sol = P.track_all(h, starts, cfg, lo=lo, hi=lo + world * B, device=local, records=records, shard=shard)
         return sol, time.perf_counter() - t0
 
-    for s in range(args.warmup):
+    # the engine's self-check (counts as the first warm-up step)
+    _, checked = validate_engine(P, h, starts, cfg, local)
+    for s in range(1, args.warmup):
         step(s)
     barrier(dist, local)
     dev_ms, wall_s, launches, paths, conv, h2d, d2h, evals, solves = 0.0, 0.0, 0, 0, 0, 0, 0, 0, 0
@@ -359,8 +403,11 @@ def run_ours(args, world, rank, local, dist):
         "scaling": "weak", "vs_baseline": None, "dtype": "dd (binary64 pairs)",
         "data": "synthetic: total-degree start solutions of cyclic-10, gamma = random_gamma(1)",
         "config": {"workload": "cyclic10 total-degree homotopy, complex double-double, TrackConfig::defaults(dd)",
-                   "paths_per_step_per_gpu": B, "chunks": "contiguous start ranges, golden-ratio spread over [0, 3628800)",
+                   "paths_per_step_per_gpu": B,
+                   "chunks": f"per step a contiguous range of {world}x{B} start indices, golden-ratio spread over "
+                             f"[0, 3628800); rank r tracks block-cyclic shard r (blocks of {SHARD_BLOCK})",
                    "parallelism": f"static path shards x{world}, no collective",
+                   "self_check": f"{checked} reference records reproduced bit for bit in a 262,144-path call before timing",
                    "l2": "working set (slot state, Jacobians) larger than L2 each step", "slots": sol_i.stats["slots"]},
         "converged_fraction": conv / max(1, paths),
         "e2e": {"value": e2e, "unit": "paths/s", "h2d_bytes_per_step": h2d // args.steps,
@@ -383,7 +430,21 @@ def main():
     ap.add_argument("--paths", type=int, default=262144, help="start paths per step per GPU")
     ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of reference CPU tracking per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="print each rank's launch geometry and shard, then exit (no GPU work)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
+    if args.launch_check:
+        world, rank, local, dist = dist_setup(cuda=False)
+        count, B = 3628800, args.paths
+        lo = chunk_offset(args.warmup, count, world * B)
+        print(json.dumps({"rank": rank, "world": world, "gpus": args.gpus, "local": local,
+                          "first_timed_step": [lo, lo + world * B], "shard": [rank, world, SHARD_BLOCK]}), flush=True)
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     world, rank, local, dist = dist_setup()
     if args.impl == "reference":
         run_reference_arm(args, world, rank)

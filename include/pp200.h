@@ -112,6 +112,7 @@ typedef struct pp_run_stats {
   double eval_ms;        /* per-kernel device time; filled only when PP200_KERNEL_TIMING=1 */
   double lsq_ms;
   double step_ms;
+  uint64_t events;       /* step events handed to the sink (pp_track_all_ex) */
 } pp_run_stats;
 
 typedef struct pp_system pp_system;     /* PolySystem (polysys.hpp:41-51) */
@@ -127,6 +128,14 @@ int pp_limbs(int prec);
 /* ---- systems: polysys.hpp:67-79 (parse_system, print_system, cyclic_system, system_stats) ---- */
 int pp_system_parse(const char* text, size_t len, pp_system** out);
 int pp_system_cyclic(uint32_t n, pp_system** out);
+/* PolySystem from its terms (polysys.hpp:21-50) without a text round trip: term_count[p] terms in
+ * polynomial p; term t has n_factors[t] (variable, exponent) pairs in `factors` (concatenated, sorted
+ * by variable, exponents >= 1) and the coefficient coeff[8t .. 8t+7] = Cplx<QD> (re limbs, im limbs).
+ * The reference host shim passes the reference's in-memory systems through this entry point. */
+int pp_system_from_terms(uint32_t dim, uint32_t n_polys, const uint32_t* term_count, const uint32_t* n_factors,
+                         const uint32_t* factors, const double* coeff, pp_system** out);
+/* CUDA devices visible to the library (0 without a usable driver) */
+int pp_device_count(void);
 /* writes a NUL-terminated text form; *needed = bytes required including the NUL */
 int pp_system_print(const pp_system* s, char* buf, size_t cap, size_t* needed);
 int pp_system_stats(const pp_system* s, uint32_t* dim, uint32_t* n_polys, uint64_t* n_monomials,
@@ -178,6 +187,51 @@ int pp_track_all(const pp_homotopy* h, const pp_starts* s, const pp_track_config
                  uint64_t lo, uint64_t hi, int device, pp_records* out, pp_run_stats* stats);
 
 /*
+ * StepEvent (tracker.hpp:62-69) and ProgressSink (tracker.hpp:70).  The reference invokes the sink
+ * once per active path and lockstep round inside step_control_all (tracker.cpp:312-315), after the
+ * step decision: t and h are the new values, newton_iters the corrector iterations of this step,
+ * status the path's status before this round's check (always PP_ACTIVE), accepted the decision.
+ * The device appends the same records to an event ring; the host hands them to the sink in
+ * batches, on the calling thread, while tracking proceeds.  Events of one path arrive in the
+ * order the reference emits them; events of different paths interleave in device order.
+ */
+typedef struct pp_step_event {
+  uint64_t path_id;
+  double t;
+  double h;
+  uint32_t newton_iters;
+  int8_t status;
+  uint8_t accepted;
+  uint8_t reserved[2];
+} pp_step_event;
+typedef void (*pp_event_sink)(const pp_step_event* events, uint64_t count, void* user);
+
+/*
+ * Block-cyclic shard of a start range (multi-GPU): start index i of [lo, hi) belongs to
+ * shard ((i - lo) / block) % count.  Interleaving blocks over the shards evens out the per-shard
+ * cost, which varies strongly with the start index.  A NULL shard (or count 1) is the whole range.
+ */
+typedef struct pp_shard {
+  uint32_t index; /* this shard, 0 <= index < count */
+  uint32_t count; /* number of shards */
+  uint64_t block; /* consecutive start indices per block (>= 1) */
+} pp_shard;
+
+/* number of start indices of [lo, hi) in shard `shard` (hi already clamped to the start count) */
+uint64_t pp_shard_size(uint64_t lo, uint64_t hi, const pp_shard* shard);
+
+/*
+ * track_all with the reference's optional arguments: `sink` (NULL = none) receives the step
+ * events (ProgressSink, tracker.hpp:166-170), and `shard` (NULL = all) restricts the call to one
+ * block-cyclic shard of [lo, min(count, hi)).  Records are written for the shard's start indices
+ * in increasing order (path_id carries the index).  pp_track_all(h, s, cfg, lo, hi, dev, out, st)
+ * equals pp_track_all_ex(h, s, cfg, lo, hi, NULL, NULL, NULL, dev, out, st).
+ */
+int pp_track_all_ex(const pp_homotopy* h, const pp_starts* s, const pp_track_config* cfg,
+                    uint64_t lo, uint64_t hi, const pp_shard* shard, pp_event_sink sink, void* sink_user,
+                    int device, pp_records* out, pp_run_stats* stats);
+
+/*
  * eval_system_batch (evaldiff.hpp:228-230) on the device for `batch` points:
  * points [batch][dim][2L], t [batch][L] -> sys [batch][n_polys][2L], jac [batch][n_polys*dim][2L]
  * (row = poly*dim + var, evaldiff.hpp:181).  jac may be NULL.
@@ -192,6 +246,14 @@ int pp_eval_batch(const pp_homotopy* h, uint32_t batch, const double* points, co
  */
 int pp_lsq_batch(int prec, uint32_t n, uint32_t batch, const double* a, const double* b,
                  double* x, uint8_t* ok, int device);
+/*
+ * The same for m x n systems (m >= n), as the reference's least_squares_solve and mgs_qr take them
+ * (linalg.hpp:79-125): a [batch][col][row][2L] with m rows, b [batch][m][2L]; optionally the
+ * factors: q [batch][col][row][2L] (Q, m x n column-major) and r [batch][n(n+1)/2][2L] (R packed by
+ * columns: row j, column i >= j at j + i(i+1)/2).  q and r may be NULL.
+ */
+int pp_lsq_batch_mn(int prec, uint32_t m, uint32_t n, uint32_t batch, const double* a, const double* b,
+                    double* x, uint8_t* ok, double* q, double* r, int device);
 
 /*
  * Output records as the reference CLI writes them (polypath_main.cpp:125-189):

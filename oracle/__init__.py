@@ -34,7 +34,9 @@ def build(reference_root: str = "/root/reference/proj") -> None:
     """Compile liboracle.so and, when the reference sources are present, _ref/libppref.so."""
     targets = ["liboracle.so"]
     if os.path.isdir(reference_root):
-        targets.append("ref")
+        # the reference library, and its acceptance suite on the CPU tracker and through the
+        # drop-in shim on libpp200.so (needs the CUDA library built first)
+        targets += ["ref", "acceptance"]
     subprocess.run(["make", "-C", HERE, "-j8", f"REF={reference_root}", *targets], check=True,
                    stdout=subprocess.DEVNULL)
 
@@ -81,6 +83,9 @@ if ref is not None:
     ref.ref_default_workers.restype = ctypes.c_uint
     ref.ref_track.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, _i32, _vp, ctypes.POINTER(TrackConfigC),
                               _u64, _u64, ctypes.POINTER(RecordsC), ctypes.POINTER(_dbl), ctypes.POINTER(_u64)]
+    ref.ref_track_events.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, _i32, _vp,
+                                     ctypes.POINTER(TrackConfigC), _u64, _u64, ctypes.POINTER(RecordsC), _vp, _u64,
+                                     ctypes.POINTER(_u64)]
     ref.ref_eval.argtypes = [ctypes.c_char_p, ctypes.c_char_p, _i32, _vp, _u32, _vp, _vp, _vp, _vp]
     ref.ref_lsq.argtypes = [_i32, _u32, _u32, _vp, _vp, _vp, _vp]
     ref.ref_td_solution.argtypes = [ctypes.c_char_p, _i32, _u64, _vp]
@@ -157,6 +162,40 @@ def ref_track(f_text: str, prec: str, gamma: complex, cfg: dict | None = None, l
     out["wall_ms"] = wall.value
     out["total_rounds"] = rounds.value
     return out
+
+
+EVENT_DTYPE = np.dtype([("path_id", np.uint64), ("t", np.float64), ("h", np.float64), ("newton_iters", np.uint32),
+                        ("status", np.int8), ("accepted", np.uint8), ("reserved", np.uint8, 2)])
+
+
+def ref_track_events(f_text: str, prec: str, gamma: complex, cfg: dict | None = None, lo: int = 0,
+                     hi: int | None = None, batch: int = 64, ev_cap: int = 1 << 20):
+    """track_all<R> of the reference with a ProgressSink collecting its StepEvents in emission order
+    (tracker.cpp:312-315); returns (records dict, events as EVENT_DTYPE array)"""
+    _need(ref, "reference build")
+    c = TrackConfigC()
+    ref.ref_track_config_defaults(PREC[prec], ctypes.byref(c))
+    for k, v in (cfg or {}).items():
+        setattr(c, k, v)
+    c.workers = 1
+    c.batch = batch
+    L = LIMBS[prec]
+    dim = int(f_text.strip().split(";")[0].split()[0])
+    cap = hi - lo
+    arrs = dict(path_id=np.zeros(cap, np.uint64), status=np.zeros(cap, np.int8), reason=np.zeros(cap, np.uint8),
+                steps=np.zeros(cap, np.uint32), newton_iters=np.zeros(cap, np.uint32),
+                rejections=np.zeros(cap, np.uint32), x=np.zeros((cap, dim, 2 * L)), residual=np.zeros((cap, L)))
+    rec = RecordsC(cap, 0, *[_ptr(arrs[k]) for k in ("path_id", "status", "reason", "steps", "newton_iters",
+                                                      "rejections", "x", "residual")])
+    g = np.array([gamma.real, gamma.imag])
+    ev = np.zeros(ev_cap, EVENT_DTYPE)
+    n_ev = _u64()
+    _chk(ref.ref_track_events(f_text.encode(), None, None, PREC[prec], _ptr(g), ctypes.byref(c), lo, hi,
+                              ctypes.byref(rec), _ptr(ev), ev_cap, ctypes.byref(n_ev)))
+    if n_ev.value > ev_cap:
+        raise RuntimeError("event capacity exceeded")
+    k = rec.count
+    return {key: v[:k].copy() for key, v in arrs.items()}, ev[:n_ev.value].copy()
 
 
 def ref_eval(f_text: str, prec: str, gamma_limbs: np.ndarray, points: np.ndarray, t: np.ndarray,

@@ -93,7 +93,7 @@ int guarded(F&& f) {
 template <class R>
 int track_impl(const char* f_text, const char* g_text, const char* starts_text, const double* gamma,
                const pp_track_config* c, uint64_t lo, uint64_t hi, pp_records* out,
-               double* wall_ms, uint64_t* rounds) {
+               double* wall_ms, uint64_t* rounds, ProgressSink* sink = nullptr) {
   PolySystem f = parse_system(f_text);
   PolySystem g;
   StartData<R> sd;
@@ -109,7 +109,7 @@ int track_impl(const char* f_text, const char* g_text, const char* starts_text, 
   auto h = make_homotopy<R>(f, g, Cplx<R>{R{gamma[0]}, R{gamma[1]}});
   TrackConfig cfg = to_cfg(c);
   auto t0 = std::chrono::steady_clock::now();
-  SolutionSet<R> sol = track_all<R>(h, sd, cfg, nullptr, lo, hi);
+  SolutionSet<R> sol = track_all<R>(h, sd, cfg, sink, lo, hi);
   double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   if (wall_ms) *wall_ms = ms;
   if (rounds) *rounds = sol.total_rounds;
@@ -354,6 +354,35 @@ int ref_track(const char* f_text, const char* g_text, const char* starts_text, i
       return track_impl<R>(f_text, g_text, starts_text, gamma, cfg, lo, hi, out, wall_ms, rounds);
     });
   });
+}
+
+// track_all<R> with a ProgressSink (tracker.hpp:62-70) that records every StepEvent in emission
+// order (tracker.cpp:312-315); *n_ev = events emitted (up to ev_cap are stored)
+int ref_track_events(const char* f_text, const char* g_text, const char* starts_text, int prec,
+                     const double* gamma, const pp_track_config* cfg, uint64_t lo, uint64_t hi,
+                     pp_records* out, pp_step_event* ev, uint64_t ev_cap, uint64_t* n_ev) {
+  uint64_t k = 0;
+  ProgressSink sink = [&](const StepEvent& e) {
+    if (k < ev_cap) {
+      pp_step_event& o = ev[k];
+      std::memset(&o, 0, sizeof o);
+      o.path_id = e.path_id;
+      o.t = e.t;
+      o.h = e.h;
+      o.newton_iters = e.newton_iters;
+      o.status = e.status;
+      o.accepted = e.accepted ? 1 : 0;
+    }
+    ++k;
+  };
+  int rc = guarded([&] {
+    return dispatch(prec, [&](auto tag) {
+      using R = decltype(tag);
+      return track_impl<R>(f_text, g_text, starts_text, gamma, cfg, lo, hi, out, nullptr, nullptr, &sink);
+    });
+  });
+  *n_ev = k;
+  return rc;
 }
 
 // eval_system_batch (evaldiff.cpp:473-488); gamma given as 2L limbs

@@ -118,7 +118,25 @@ class RunStatsC(ctypes.Structure):
         ("eval_ms", ctypes.c_double),
         ("lsq_ms", ctypes.c_double),
         ("step_ms", ctypes.c_double),
+        ("events", ctypes.c_uint64),
     ]
+
+
+class ShardC(ctypes.Structure):
+    _fields_ = [("index", ctypes.c_uint32), ("count", ctypes.c_uint32), ("block", ctypes.c_uint64)]
+
+
+class StepEventC(ctypes.Structure):
+    """StepEvent (tracker.hpp:62-69), pp_step_event"""
+    _fields_ = [("path_id", ctypes.c_uint64), ("t", ctypes.c_double), ("h", ctypes.c_double),
+                ("newton_iters", ctypes.c_uint32), ("status", ctypes.c_int8), ("accepted", ctypes.c_uint8),
+                ("reserved", ctypes.c_uint8 * 2)]
+
+
+EVENT_DTYPE = np.dtype([("path_id", np.uint64), ("t", np.float64), ("h", np.float64), ("newton_iters", np.uint32),
+                        ("status", np.int8), ("accepted", np.uint8), ("reserved", np.uint8, 2)])
+assert EVENT_DTYPE.itemsize == ctypes.sizeof(StepEventC) == 32
+EventSinkFn = ctypes.CFUNCTYPE(None, ctypes.POINTER(StepEventC), ctypes.c_uint64, ctypes.c_void_p)
 
 
 _vp = ctypes.c_void_p
@@ -139,6 +157,8 @@ _sig("pp_last_error", ctypes.c_char_p)
 _sig("pp_limbs", _i32, _i32)
 _sig("pp_system_parse", _i32, ctypes.c_char_p, _sz, _P(_vp))
 _sig("pp_system_cyclic", _i32, _u32, _P(_vp))
+_sig("pp_system_from_terms", _i32, _u32, _u32, _vp, _vp, _vp, _vp, _P(_vp))
+_sig("pp_device_count", _i32)
 _sig("pp_system_print", _i32, _vp, ctypes.c_char_p, _sz, _P(_sz))
 _sig("pp_system_stats", _i32, _vp, _P(_u32), _P(_u32), _P(_u64), _P(_u64), _P(_i32))
 _sig("pp_system_degrees", _i32, _vp, _vp)
@@ -158,12 +178,16 @@ _sig("pp_homotopy_free", None, _vp)
 _sig("pp_track_config_defaults", None, _i32, _P(TrackConfigC))
 _sig("pp_track_config_validate", _i32, _P(TrackConfigC))
 _sig("pp_track_all", _i32, _vp, _vp, _P(TrackConfigC), _u64, _u64, _i32, _P(RecordsC), _P(RunStatsC))
+_sig("pp_track_all_ex", _i32, _vp, _vp, _P(TrackConfigC), _u64, _u64, _P(ShardC), EventSinkFn, _vp, _i32, _P(RecordsC),
+     _P(RunStatsC))
+_sig("pp_shard_size", _u64, _u64, _u64, _P(ShardC))
 _sig("pp_solutions_jsonl", _i32, _vp, _i32, _u32, _vp, _u64, ctypes.c_char_p, _dbl, _u64, _u64, ctypes.c_char_p,
      _sz, _P(_sz))
 _sig("pp_to_decimal", _i32, _i32, _vp, ctypes.c_char_p, _sz)
 _sig("pp_bench_eval", _i32, _vp, _u64, _u32, _u32, _i32, _P(_dbl), _P(_u64))
 _sig("pp_eval_batch", _i32, _vp, _u32, _vp, _vp, _vp, _vp, _i32)
 _sig("pp_lsq_batch", _i32, _i32, _u32, _u32, _vp, _vp, _vp, _vp, _i32)
+_sig("pp_lsq_batch_mn", _i32, _i32, _u32, _u32, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _i32)
 _sig("pp_test_arith", _i32, _i32, _i32, _vp, _vp, _vp)
 _sig("pp_test_parse_decimal", _i32, _i32, ctypes.c_char_p, _vp)
 _sig("pp_test_to_decimal", _i32, _i32, _vp, ctypes.c_char_p, _sz)
@@ -177,7 +201,7 @@ EXPORTED = [
     "pp_load_start_data", "pp_starts_explicit", "pp_starts_roots", "pp_starts_count", "pp_starts_solution", "pp_starts_free",
     "pp_make_homotopy", "pp_homotopy_info", "pp_homotopy_free", "pp_track_config_defaults",
     "pp_track_config_validate", "pp_track_all", "pp_eval_batch", "pp_lsq_batch", "pp_solutions_jsonl",
-    "pp_to_decimal", "pp_bench_eval",
+    "pp_to_decimal", "pp_bench_eval", "pp_track_all_ex", "pp_shard_size", "pp_system_from_terms", "pp_device_count", "pp_lsq_batch_mn",
 ]
 
 
@@ -252,6 +276,34 @@ def cyclic_system(n: int) -> System:
     h = _vp()
     _check(lib.pp_system_cyclic(n, ctypes.byref(h)))
     return System(h.value)
+
+
+def system_from_terms(dim: int, polys) -> System:
+    """PolySystem from terms without a text round trip (pp_system_from_terms): polys is a list of
+    polynomials, each a list of (coeff, [(var, exp), ...]) with coeff a complex or 8 QD limbs
+    (re limbs, im limbs)."""
+    counts, nf, fac, co = [], [], [], []
+    for poly in polys:
+        counts.append(len(poly))
+        for c, mono in poly:
+            limbs = np.zeros(8)
+            if np.isscalar(c):
+                limbs[0], limbs[4] = complex(c).real, complex(c).imag
+            else:
+                limbs[:] = np.asarray(c, dtype=np.float64)
+            co.append(limbs)
+            nf.append(len(mono))
+            for v, e in mono:
+                fac += [v, e]
+    arrs = [np.asarray(counts, np.uint32), np.asarray(nf, np.uint32), np.asarray(fac or [0], np.uint32),
+            np.asarray(co if co else np.zeros((1, 8)), np.float64)]
+    out = _vp()
+    _check(lib.pp_system_from_terms(dim, len(polys), *[_ptr(a) for a in arrs], ctypes.byref(out)))
+    return System(out.value)
+
+
+def device_count() -> int:
+    return int(lib.pp_device_count())
 
 
 def random_gamma(seed: int) -> complex:
@@ -513,18 +565,48 @@ class Records:
                            self.x[:k].copy(), self.residual[:k].copy(), stats)
 
 
+def shard_size(lo: int, hi: int, shard: tuple[int, int, int] | None) -> int:
+    """number of start indices of [lo, hi) in the block-cyclic shard (index, count, block)"""
+    sh = ShardC(*shard) if shard is not None else None
+    return int(lib.pp_shard_size(lo, hi, ctypes.byref(sh) if sh is not None else None))
+
+
 def track_all(h: Homotopy, starts: Starts, cfg: TrackConfig | None = None, lo: int = 0, hi: int | None = None,
-              device: int = 0, records: Records | None = None) -> SolutionSet:
-    """track_all<R> (tracker.hpp:166-170) on CUDA device `device`: starts [lo, min(count, hi))."""
+              device: int = 0, records: Records | None = None, sink=None,
+              shard: tuple[int, int, int] | None = None) -> SolutionSet:
+    """track_all<R> (tracker.hpp:166-170) on CUDA device `device`: starts [lo, min(count, hi)).
+
+    sink: the ProgressSink (tracker.hpp:70), called with numpy arrays of EVENT_DTYPE (batches of
+    StepEvents, tracker.hpp:62-69) while tracking proceeds.  shard: (index, count, block) restricts
+    the call to one block-cyclic shard of the range (pp_shard), for multi-GPU partitions."""
     cfg = cfg or TrackConfig.defaults(h.prec)
     count = starts.count
     end = count if hi is None else min(count, hi)
-    cap = max(0, end - lo)
-    rec = records if records is not None else Records(max(cap, 1), starts.dim, h.prec)
+    cap = shard_size(lo, end, shard) if end > lo else 0
+    if records is not None:
+        if records.prec != h.prec or records.x.shape[1:] != (starts.dim, 2 * LIMBS[h.prec]):
+            raise InvalidArgument("track_all: records were allocated for another dimension or precision")
+        rec = records
+    else:
+        rec = Records(max(cap, 1), starts.dim, h.prec)
     c = cfg.to_c()
     st = RunStatsC()
-    _check(lib.pp_track_all(h._h, starts._h, ctypes.byref(c), lo, end if hi is not None else (1 << 64) - 1, device,
-                            ctypes.byref(rec.c), ctypes.byref(st)))
+    sh = ShardC(*shard) if shard is not None else None
+    errors = []
+
+    def _on_events(ptr, n, _user):
+        try:
+            buf = (ctypes.c_char * (int(n) * EVENT_DTYPE.itemsize)).from_address(ctypes.addressof(ptr.contents))
+            sink(np.frombuffer(buf, dtype=EVENT_DTYPE).copy())
+        except BaseException as exc:  # noqa: BLE001 -- re-raised after the call returns
+            errors.append(exc)
+
+    cb = EventSinkFn(_on_events) if sink is not None else EventSinkFn()
+    _check(lib.pp_track_all_ex(h._h, starts._h, ctypes.byref(c), lo, end if hi is not None else (1 << 64) - 1,
+                               ctypes.byref(sh) if sh is not None else None, cb, None, device, ctypes.byref(rec.c),
+                               ctypes.byref(st)))
+    if errors:
+        raise errors[0]
     stats = {f[0]: getattr(st, f[0]) for f in RunStatsC._fields_}
     return rec.solution_set(stats)
 
@@ -572,6 +654,22 @@ def lsq_batch(prec, a: np.ndarray, b: np.ndarray, device: int = 0):
     ok = np.zeros(B, dtype=np.uint8)
     _check(lib.pp_lsq_batch(_prec(prec), n, B, _ptr(a), _ptr(b), _ptr(x), _ptr(ok), device))
     return x, ok.astype(bool)
+
+
+def lsq_batch_mn(prec, a: np.ndarray, b: np.ndarray, device: int = 0, factors: bool = False):
+    """least_squares_solve / mgs_qr (linalg.hpp:79-125) for m x n systems (m >= n), batched:
+    a [B][n(col)][m(row)][2L], b [B][m][2L] -> x [B][n][2L], ok [B] (and with factors=True the
+    Q factor [B][n][m][2L] and R packed by columns [B][n(n+1)/2][2L])."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    B, n, m, w = a.shape
+    x = np.zeros((B, n, w))
+    ok = np.zeros(B, dtype=np.uint8)
+    q = np.zeros_like(a) if factors else None
+    r = np.zeros((B, n * (n + 1) // 2, w)) if factors else None
+    _check(lib.pp_lsq_batch_mn(_prec(prec), m, n, B, _ptr(a), _ptr(b), _ptr(x), _ptr(ok),
+                               _ptr(q) if factors else None, _ptr(r) if factors else None, device))
+    return (x, ok.astype(bool), q, r) if factors else (x, ok.astype(bool))
 
 
 def fp64_peak(device: int = 0) -> float:

@@ -81,7 +81,9 @@ void need(bool cond, const char* msg) {
 
 extern "C" {
 
-const char* pp_version(void) { return "pp200 0.1 (sm_100a)"; }
+const char* pp_version(void) { return "pp200 0.2 (sm_100a)"; }
+
+int pp_device_count(void) { return pp::device_count(); }
 const char* pp_last_error(void) { return g_error.c_str(); }
 int pp_limbs(int prec) { return limbs_of(prec); }
 
@@ -90,6 +92,36 @@ int pp_system_parse(const char* text, size_t len, pp_system** out) {
     need(text != nullptr && out != nullptr, "pp_system_parse: null argument");
     auto s = std::make_unique<pp_system>();
     s->sys = pp::parse_system(std::string_view(text, len));
+    *out = s.release();
+    return PP_OK;
+  });
+}
+
+int pp_system_from_terms(uint32_t dim, uint32_t n_polys, const uint32_t* term_count, const uint32_t* n_factors,
+                         const uint32_t* factors, const double* coeff, pp_system** out) {
+  return guard([&] {
+    need(out != nullptr && (n_polys == 0 || term_count != nullptr), "pp_system_from_terms: null argument");
+    need(n_polys > 0, "system has no polynomials");
+    auto s = std::make_unique<pp_system>();
+    s->sys.dim = dim;
+    s->sys.polys.resize(n_polys);
+    size_t t = 0, f = 0;
+    for (uint32_t p = 0; p < n_polys; ++p) {
+      for (uint32_t i = 0; i < term_count[p]; ++i, ++t) {
+        pp::Term term;
+        const double* c = coeff + t * 8;
+        term.coeff = pp::cqd{pp::qd_t{c[0], c[1], c[2], c[3]}, pp::qd_t{c[4], c[5], c[6], c[7]}};
+        for (uint32_t k = 0; k < n_factors[t]; ++k, ++f) {
+          const uint32_t var = factors[2 * f], e = factors[2 * f + 1];
+          need(var < dim && e >= 1, "pp_system_from_terms: bad factor");
+          need(term.mono.factors.empty() || term.mono.factors.back().first < var,
+               "pp_system_from_terms: factors must be sorted by variable");
+          term.mono.factors.emplace_back(var, e);
+        }
+        s->sys.polys[p].push_back(std::move(term));
+      }
+    }
+    s->sys.refresh_degrees();
     *out = s.release();
     return PP_OK;
   });
@@ -393,8 +425,15 @@ int pp_track_config_validate(const pp_track_config* c) {
   });
 }
 
-int pp_track_all(const pp_homotopy* h, const pp_starts* s, const pp_track_config* cfg, uint64_t lo,
-                 uint64_t hi, int device, pp_records* out, pp_run_stats* stats) {
+uint64_t pp_shard_size(uint64_t lo, uint64_t hi, const pp_shard* shard) {
+  pp::TrackShard sh;
+  if (shard != nullptr && shard->count > 1) sh = {shard->index, shard->count, shard->block ? shard->block : 1};
+  return pp::shard_size(lo, hi, sh);
+}
+
+int pp_track_all_ex(const pp_homotopy* h, const pp_starts* s, const pp_track_config* cfg, uint64_t lo,
+                    uint64_t hi, const pp_shard* shard, pp_event_sink sink, void* sink_user, int device,
+                    pp_records* out, pp_run_stats* stats) {
   int rc = pp_track_config_validate(cfg);
   if (rc != PP_OK) return rc;
   return guard([&] {
@@ -403,15 +442,28 @@ int pp_track_all(const pp_homotopy* h, const pp_starts* s, const pp_track_config
     need(s->st.prec == h->plan.prec, "track_all: start data and homotopy precision differ");
     need(s->st.dim == h->plan.dim, "track_all: start dimension differs from the homotopy");
     need(h->plan.n_polys == h->plan.dim, "track_all: the homotopy must be square");
+    pp::TrackShard sh;
+    if (shard != nullptr) {
+      need(shard->count >= 1 && shard->index < shard->count && shard->block >= 1, "track_all: bad shard");
+      sh = {shard->index, shard->count, shard->block};
+    }
     const uint64_t end = std::min<uint64_t>(s->st.count, hi);
     if (stats) std::memset(stats, 0, sizeof *stats);
     out->count = 0;
     if (lo >= end) return PP_OK;
-    if (out->capacity < end - lo) return PP_E_CAPACITY;
+    const uint64_t n = pp::shard_size(lo, end, sh);
+    if (n == 0) return PP_OK;
+    if (out->capacity < n) return PP_E_CAPACITY;
     pp_homotopy* hm = const_cast<pp_homotopy*>(h);
-    pp::device_track(hm->plan, hm->on(device), s->st, *cfg, lo, end, device, out, stats);
+    pp::device_track(hm->plan, hm->on(device), s->st, *cfg, lo, end, sh, pp::EventSink{sink, sink_user}, device, out,
+                     stats);
     return PP_OK;
   });
+}
+
+int pp_track_all(const pp_homotopy* h, const pp_starts* s, const pp_track_config* cfg, uint64_t lo,
+                 uint64_t hi, int device, pp_records* out, pp_run_stats* stats) {
+  return pp_track_all_ex(h, s, cfg, lo, hi, nullptr, nullptr, nullptr, device, out, stats);
 }
 
 int pp_eval_batch(const pp_homotopy* h, uint32_t batch, const double* points, const double* t, double* sys,
@@ -424,14 +476,19 @@ int pp_eval_batch(const pp_homotopy* h, uint32_t batch, const double* points, co
   });
 }
 
-int pp_lsq_batch(int prec, uint32_t n, uint32_t batch, const double* a, const double* b, double* x, uint8_t* ok,
-                 int device) {
+int pp_lsq_batch_mn(int prec, uint32_t m, uint32_t n, uint32_t batch, const double* a, const double* b, double* x,
+                    uint8_t* ok, double* q, double* r, int device) {
   return guard([&] {
-    need(limbs_of(prec) > 0 && n >= 1, "pp_lsq_batch: bad argument");
+    need(limbs_of(prec) > 0 && n >= 1 && m >= n, "pp_lsq_batch: bad argument (need m >= n >= 1)");
     need(batch == 0 || (a && b && x && ok), "pp_lsq_batch: null argument");
-    pp::device_lsq(prec, n, batch, a, b, x, ok, device);
+    pp::device_lsq(prec, m, n, batch, a, b, x, ok, q, r, device);
     return PP_OK;
   });
+}
+
+int pp_lsq_batch(int prec, uint32_t n, uint32_t batch, const double* a, const double* b, double* x, uint8_t* ok,
+                 int device) {
+  return pp_lsq_batch_mn(prec, n, n, batch, a, b, x, ok, nullptr, nullptr, device);
 }
 
 // ---- output records: the reference CLI's JSON lines (polypath_main.cpp:125-189) ----

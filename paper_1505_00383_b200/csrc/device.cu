@@ -10,6 +10,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
+#include <tuple>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -32,6 +34,37 @@ T* dmalloc(size_t count) {
   check(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
   return static_cast<T*>(p);
 }
+
+// a pair of timing events, destroyed on every path
+struct EvPair {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  EvPair() {
+    check(cudaEventCreate(&e0), "event");
+    check(cudaEventCreate(&e1), "event");
+  }
+  EvPair(const EvPair&) = delete;
+  EvPair& operator=(const EvPair&) = delete;
+  ~EvPair() {
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+  }
+};
+
+// device buffer owned for the duration of a kernel-level call (freed on every path)
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  explicit DevBuf(size_t count) { p = dmalloc<T>(count); }
+  explicit DevBuf(const std::vector<T>& v) {
+    p = dmalloc<T>(v.size());
+    if (!v.empty()) check(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
 
 template <class T>
 T* upload(const std::vector<T>& v) {
@@ -74,25 +107,152 @@ const dev::Variant* pick_variant(int prec, uint32_t n, uint32_t max_k) {
   return best;
 }
 
-// grow-only scratch arena per (calling host thread, device): concurrent track_all calls from
-// different host threads (each on its own stream) never share a workspace
-struct Arena {
-  void* ptr = nullptr;
-  size_t bytes = 0;
-};
-thread_local std::map<int, Arena> t_arenas;
+// Per (calling host thread, device) context, reused across calls: a grow-only workspace, the
+// stream, timing events, a pinned mailbox and the pinned step-event staging buffer.  Concurrent
+// track_all calls from different host threads (each on its own stream) never share one.
+struct Ctx {
+  int device = -1;
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {};   // call phases: H2D, trips, D2H
+  cudaEvent_t kev[4] = {};  // instrumented trips
+  unsigned long long* mbox = nullptr;
+  void* ev_host = nullptr;
+  size_t ev_host_bytes = 0;
 
-void* arena(int device, size_t bytes) {
-  Arena& a = t_arenas[device];
-  if (a.bytes < bytes) {
-    if (a.ptr) cudaFree(a.ptr);
-    a.ptr = nullptr;
-    a.bytes = 0;
-    check(cudaMalloc(&a.ptr, bytes), "cudaMalloc(workspace)");
-    a.bytes = bytes;
+  explicit Ctx(int dev) : device(dev) {
+    check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
+    for (auto& e : ev) check(cudaEventCreate(&e), "event");
+    for (auto& e : kev) check(cudaEventCreate(&e), "event");
+    check(cudaMallocHost(&mbox, 4 * sizeof(unsigned long long)), "cudaMallocHost");
   }
-  return a.ptr;
+  Ctx(const Ctx&) = delete;
+  Ctx& operator=(const Ctx&) = delete;
+  ~Ctx() {
+    // best effort (the runtime may already be shutting down at thread / process exit)
+    int prev = -1;
+    if (cudaGetDevice(&prev) != cudaSuccess) return;
+    cudaSetDevice(device);
+    if (ws) cudaFree(ws);
+    if (ev_host) cudaFreeHost(ev_host);
+    if (mbox) cudaFreeHost(mbox);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : kev)
+      if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+    cudaSetDevice(prev);
+  }
+  void* workspace(size_t bytes) {
+    if (ws_bytes < bytes) {
+      check(cudaStreamSynchronize(stream), "workspace");
+      if (ws) cudaFree(ws);
+      ws = nullptr;
+      ws_bytes = 0;
+      check(cudaMalloc(&ws, bytes), "cudaMalloc(workspace)");
+      ws_bytes = bytes;
+    }
+    return ws;
+  }
+  void* event_staging(size_t bytes) {
+    if (ev_host_bytes < bytes) {
+      if (ev_host) cudaFreeHost(ev_host);
+      ev_host = nullptr;
+      ev_host_bytes = 0;
+      check(cudaMallocHost(&ev_host, bytes), "cudaMallocHost(events)");
+      ev_host_bytes = bytes;
+    }
+    return ev_host;
+  }
+};
+thread_local std::map<int, std::unique_ptr<Ctx>> t_ctx;
+
+Ctx& context(int device) {
+  auto& p = t_ctx[device];
+  if (!p) p = std::make_unique<Ctx>(device);
+  return *p;
 }
+
+// device properties, queried once per device
+const cudaDeviceProp& device_props(int device) {
+  static std::mutex mu;
+  static std::map<int, cudaDeviceProp> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(device);
+  if (it == cache.end()) {
+    cudaDeviceProp p;
+    check(cudaGetDeviceProperties(&p, device), "cudaGetDeviceProperties");
+    it = cache.emplace(device, p).first;
+  }
+  return it->second;
+}
+
+// The dynamic shared memory limit of a kernel is raised, never lowered, under a lock: concurrent
+// calls for systems of different sizes share kernels, and lowering the limit between another
+// thread's check and its launch (or graph capture) would fail that launch.
+void ensure_smem(const void* fn, size_t bytes, int device) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> cur;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& c = cur[{device, fn}];
+  if (bytes <= c) return;
+  check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)),
+        "cudaFuncSetAttribute");
+  c = bytes;
+}
+
+int occupancy(const void* fn, int block, size_t smem, int device) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, int, size_t>, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_tuple(device, fn, block, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int per_sm = 0;
+  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem), "occupancy");
+  cache[key] = per_sm;
+  return per_sm;
+}
+
+// scope guards of one tracking call
+struct AsyncTemps {  // stream-ordered temporary allocations
+  cudaStream_t stream;
+  std::vector<void*> ptrs;
+  void* alloc(size_t b) {
+    void* p = nullptr;
+    check(cudaMallocAsync(&p, b, stream), "cudaMallocAsync");
+    ptrs.push_back(p);
+    return p;
+  }
+  void release() {
+    for (void* p : ptrs) cudaFreeAsync(p, stream);
+    ptrs.clear();
+  }
+  ~AsyncTemps() { release(); }
+};
+struct GraphHolder {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  void reset() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    exec = nullptr;
+    graph = nullptr;
+  }
+  ~GraphHolder() { reset(); }
+};
+struct CaptureGuard {  // ends a capture an exception interrupted, so the stream stays usable
+  cudaStream_t stream;
+  bool active = false;
+  ~CaptureGuard() {
+    if (!active) return;
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(stream, &g);
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+  }
+};
 
 size_t align_up(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
@@ -141,7 +301,25 @@ dev::PlanArgs plan_args(const Plan& plan, const DevicePlan* dp) {
 }
 }  // namespace
 
+int device_count() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
 bool device_supports(uint32_t n, uint32_t max_k) { return pick_variant(1, n, max_k) != nullptr; }
+
+uint64_t shard_size(uint64_t lo, uint64_t hi, const TrackShard& sh) {
+  if (hi <= lo) return 0;
+  const uint64_t total = hi - lo;
+  if (sh.count <= 1) return total;
+  const uint64_t span = sh.block * sh.count, full = total / span, rem = total % span;
+  const uint64_t first = sh.index * sh.block;
+  return full * sh.block + (rem > first ? std::min<uint64_t>(sh.block, rem - first) : 0);
+}
 
 // ---------------------------------------------------------------------------------------------
 // FP64 pipe throughput microbenchmark: the roofline denominator for the FP64-bound kernels.
@@ -218,21 +396,16 @@ double device_fp64_peak(int device) {
   check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
   const int block = 256, per_sm = 8, iters = 1 << 14;
   const int blocks = prop.multiProcessorCount * per_sm;
-  double* out = dmalloc<double>(blocks);
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
-  fp64_peak_kernel<<<blocks, block>>>(out, iters);  // warm-up
-  cudaEventRecord(e0);
+  DevBuf<double> out(blocks);
+  EvPair ev;
+  fp64_peak_kernel<<<blocks, block>>>(out.p, iters);  // warm-up
+  check(cudaEventRecord(ev.e0), "event");
   const int reps = 5;
-  for (int r = 0; r < reps; ++r) fp64_peak_kernel<<<blocks, block>>>(out, iters);
-  cudaEventRecord(e1);
-  check(cudaEventSynchronize(e1), "fp64 peak kernel");
+  for (int r = 0; r < reps; ++r) fp64_peak_kernel<<<blocks, block>>>(out.p, iters);
+  check(cudaEventRecord(ev.e1), "event");
+  check(cudaEventSynchronize(ev.e1), "fp64 peak kernel");
   float ms = 0;
-  cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  cudaFree(out);
+  check(cudaEventElapsedTime(&ms, ev.e0, ev.e1), "event time");
   const double ops = static_cast<double>(reps) * blocks * block * iters * 8.0;
   return ops / (ms / 1e3);
 }
@@ -282,17 +455,17 @@ size_t env_size(const char* name, size_t dflt) {
 }
 
 void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_track_config& cfg,
-                  uint64_t lo, uint64_t hi, int device, pp_records* out, pp_run_stats* stats) {
+                  uint64_t lo, uint64_t hi, const TrackShard& shard, const EventSink& sink, int device,
+                  pp_records* out, pp_run_stats* stats) {
   auto wall0 = std::chrono::steady_clock::now();
   DeviceGuard g(device);
   const uint32_t n = plan.dim;
   const uint32_t L = plan.L;
   const dev::Variant* var = pick_variant(plan.prec, n, plan.max_k);
   if (var == nullptr) throw InvalidArgument("system dimension / monomial size beyond the compiled kernels (KMAX 16; n <= 97 in dd)");
-  const uint64_t count = hi - lo;
+  const uint64_t count = shard_size(lo, hi, shard);  // records of this call
 
-  cudaDeviceProp prop;
-  check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  const cudaDeviceProp& prop = device_props(device);
   const size_t per_thread_smem = static_cast<size_t>(2) * n * 2 * L * sizeof(double);
   int tblock = static_cast<int>(std::min<size_t>(128, std::max<size_t>(32, env_size("PP200_TRIP_BLOCK", kBlock))));
   while (tblock > 32 && static_cast<size_t>(tblock) * per_thread_smem > 200 * 1024) tblock /= 2;
@@ -308,30 +481,33 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   while (tmem_cols < static_cast<uint32_t>(n) * 4 * L) tmem_cols *= 2;
   if (tmem) {
     // every resident CTA must get its columns at once (512 per SM), or tcgen05.alloc would stall
-    int per_sm = 0;
-    check(cudaFuncSetAttribute(var->ctrl_eval_tmem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(eblock * per_thread_smem / 2)), "cudaFuncSetAttribute");
-    check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var->ctrl_eval_tmem, eblock, eblock * per_thread_smem / 2),
-          "occupancy");
-    tmem = static_cast<uint32_t>(per_sm) * tmem_cols <= 512;
+    ensure_smem(var->ctrl_eval_tmem, eblock * per_thread_smem / 2, device);
+    tmem = static_cast<uint32_t>(occupancy(var->ctrl_eval_tmem, eblock, eblock * per_thread_smem / 2, device)) *
+               tmem_cols <= 512;
   }
   const void* ctrl_eval_fn = tmem ? var->ctrl_eval_tmem : var->ctrl_eval_trip;
   const size_t eval_smem = static_cast<size_t>(eblock) * per_thread_smem / (tmem ? 2 : 1);
   // least squares: the column being orthogonalised in shared memory, or (PP200_LSQ_TMEM=1, n*4L <= 128)
   // in tensor memory with 256-thread CTAs, two per SM (256 TMEM columns each), leaving L1 to Q
   bool lsq_tm = env_size("PP200_LSQ_TMEM", 0) != 0 && static_cast<size_t>(n) * 4 * L <= 128 && tblock == 128;
-  if (lsq_tm) {
-    int per_sm = 0;
-    check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var->lsq_tmem, 256, 0), "occupancy");
-    lsq_tm = per_sm <= 2;  // more resident CTAs than TMEM columns would stall in tcgen05.alloc
-  }
+  if (lsq_tm) lsq_tm = occupancy(var->lsq_tmem, 256, 0, device) <= 2;  // more CTAs than TMEM columns would stall
   const void* lsq_fn = lsq_tm ? var->lsq_tmem : var->lsq_trip;
+  // register-resident solver for the compiled dimensions (PP200_LSQ_REG: 0 off, 1 stream, 2 hold q_i;
+  // default 2 in complex double, where it halves the solver's HBM traffic: lsq 0.86 -> 0.53 s on
+  // 262,144 cyclic-10 paths)
+  const void* lsq_reg = nullptr;
+  if (!lsq_tm && tblock == 128 && plan.prec <= 1) {
+    const size_t mode = env_size("PP200_LSQ_REG", plan.prec == 0 ? 2 : 0);
+    int cnt = 0;
+    const dev::LsqReg* lr = plan.prec == 0 ? dev::lsq_reg_d(&cnt) : dev::lsq_reg_dd(&cnt);
+    for (int i = 0; i < cnt && mode != 0; ++i)
+      if (lr[i].n == static_cast<int>(n)) lsq_reg = mode == 1 ? lr[i].stream : lr[i].hold;
+  }
+  if (lsq_reg) lsq_fn = lsq_reg;
   const int lblock = lsq_tm ? 256 : tblock;
-  const size_t lsq_smem = lsq_tm ? 0 : static_cast<size_t>(tblock) * per_thread_smem / 2;
-  check(cudaFuncSetAttribute(ctrl_eval_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(eval_smem)),
-        "cudaFuncSetAttribute");
-  check(cudaFuncSetAttribute(lsq_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsq_smem)),
-        "cudaFuncSetAttribute");
+  const size_t lsq_smem = (lsq_tm || lsq_reg) ? 0 : static_cast<size_t>(tblock) * per_thread_smem / 2;
+  ensure_smem(ctrl_eval_fn, eval_smem, device);
+  ensure_smem(lsq_fn, lsq_smem, device);
   // slots: PP200_SLOTS_PER_SM per SM (default 512; 1024 in complex double, whose kernels are
   // memory-latency bound and want more warps), never more than the paths (whole blocks)
   const size_t per_sm = std::max<size_t>(tblock, env_size("PP200_SLOTS_PER_SM", L == 1 ? 1024 : 512));
@@ -348,6 +524,8 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   const size_t nJ = static_cast<size_t>(n) * n, nR = static_cast<size_t>(n) * (n + 1) / 2;
   const size_t kH = dev::kHistDepth;
   const size_t graph_trips = std::max<size_t>(1, env_size("PP200_GRAPH_TRIPS", 16));
+  // step events: at most one per busy slot and trip, so graph_trips * S per drain
+  const uint64_t ev_cap = sink.fn ? static_cast<uint64_t>(graph_trips) * S : 0;
   size_t bytes = 0;
   auto room = [&](size_t b) { bytes += align_up(b); };
   room(dev::kIntFields * S * 4);
@@ -370,7 +548,10 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   room(count);
   room(64);
   room(graph_trips * 4);
-  Carver cv{static_cast<char*>(arena(device, bytes))};
+  room(ev_cap * sizeof(dev::StepEventRec));
+  room((2 * S + 2) * sizeof(unsigned));  // compaction lists
+  Ctx& cx = context(device);
+  Carver cv{static_cast<char*>(cx.workspace(bytes))};
 
   dev::TrackArgs a{};
   a.plan = plan_args(plan, dp);
@@ -389,6 +570,10 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   a.max_steps = cfg.max_steps;
   a.lo = lo;
   a.hi = hi;
+  a.count = count;
+  a.shard_block = shard.count > 1 ? shard.block : 1;
+  a.shard_n = shard.count > 1 ? shard.count : 1;
+  a.shard_r = shard.count > 1 ? shard.index : 0;
   a.S = S;
   a.si = cv.take<int32_t>(dev::kIntFields * S);
   a.spath = cv.take<unsigned long long>(S);
@@ -413,62 +598,59 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   a.rec_divflag = cv.take<uint8_t>(count);
   a.next = cv.take<unsigned long long>(8);
   a.work = a.next + 2;
+  a.ev_count = a.next + 4;
   unsigned* busy = cv.take<unsigned>(graph_trips);
+  a.ev = ev_cap ? cv.take<dev::StepEventRec>(ev_cap) : nullptr;
+  a.ev_cap = ev_cap;
+  unsigned* holes = cv.take<unsigned>(2 * S + 2);
+  dev::StepEventRec* ev_host = ev_cap ? static_cast<dev::StepEventRec*>(cx.event_staging(ev_cap * sizeof(dev::StepEventRec)))
+                                      : nullptr;
 
-  cudaStream_t stream;
-  check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
-  // PP200_L2_PERSIST=1: mark the solver's Jacobian/Q array as L2-persisting for the fraction that
-  // fits the device's persisting-L2 limit (the rest streams), so part of the slots re-read their Q
-  // from L2 instead of HBM on every projection
-  const bool l2_persist = env_size("PP200_L2_PERSIST", 0) != 0;
-  if (l2_persist && prop.persistingL2CacheMaxSize > 0) {
-    const size_t jbytes = nJ * cw * S * sizeof(double);
-    check(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, prop.persistingL2CacheMaxSize), "L2 limit");
-    cudaStreamAttrValue attr{};
-    attr.accessPolicyWindow.base_ptr = a.J;
-    attr.accessPolicyWindow.num_bytes = std::min<size_t>(jbytes, prop.accessPolicyMaxWindowSize);
-    attr.accessPolicyWindow.hitRatio = std::min<float>(
-        1.0f, static_cast<float>(prop.persistingL2CacheMaxSize) / static_cast<float>(attr.accessPolicyWindow.num_bytes));
-    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    check(cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &attr), "access policy");
-  }
-  cudaEvent_t e0, e1, e2, e3;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
-  cudaEventCreate(&e2);
-  cudaEventCreate(&e3);
+  cudaStream_t stream = cx.stream;
+  cudaEvent_t* e = cx.ev;  // e[0] H2D e[1] trips e[2] D2H e[3]
+  unsigned long long* mbox = cx.mbox;  // pinned: [0] busy slots, [1] start counter, [2] events
+  AsyncTemps temps{stream};
+  GraphHolder gh;
+  CaptureGuard capg{stream};
 
   // start tables (small): uploaded per call; explicit start lists only for [lo, hi)
-  std::vector<void*> temps;
   uint64_t h2d = 0;
   auto up = [&](const void* src, size_t b) -> void* {
-    void* p = nullptr;
-    check(cudaMallocAsync(&p, b == 0 ? 1 : b, stream), "cudaMallocAsync");
+    void* p = temps.alloc(b == 0 ? 1 : b);
     if (b) check(cudaMemcpyAsync(p, src, b, cudaMemcpyHostToDevice, stream), "H2D");
-    temps.push_back(p);
     h2d += b;
     return p;
   };
-  cudaEventRecord(e0, stream);
+  check(cudaEventRecord(e[0], stream), "event");
   if (st.total_degree) {
     a.degrees = static_cast<const uint32_t*>(up(st.degrees.data(), st.degrees.size() * 4));
     a.root_off = static_cast<const uint32_t*>(up(st.root_off.data(), st.root_off.size() * 4));
     a.roots = static_cast<const double*>(up(st.roots.data(), st.roots.size() * 8));
   } else {
-    a.explicit_x = static_cast<const double*>(up(st.explicit_x.data() + lo * n * cw, count * n * cw * 8));
+    a.explicit_x = static_cast<const double*>(up(st.explicit_x.data() + lo * n * cw, (hi - lo) * n * cw * 8));
   }
-  cudaEventRecord(e1, stream);
+  check(cudaEventRecord(e[1], stream), "event");
   check(cudaMemsetAsync(a.si, 0, dev::kIntFields * S * 4, stream), "memset");  // all slots M_IDLE
   check(cudaMemsetAsync(a.next, 0, 8 * sizeof(unsigned long long), stream), "memset");
 
+  // hand the step events produced so far to the sink and reset the ring (stream is idle here)
+  uint64_t n_events = 0;
+  auto drain_events = [&]() {
+    if (!ev_cap) return;
+    check(cudaMemcpyAsync(mbox + 2, a.ev_count, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream), "D2H");
+    check(cudaStreamSynchronize(stream), "events");
+    const uint64_t ne = mbox[2];
+    if (ne > ev_cap) throw CudaFailure("step-event ring overflow");
+    if (ne == 0) return;
+    check(cudaMemcpyAsync(ev_host, a.ev, ne * sizeof(dev::StepEventRec), cudaMemcpyDeviceToHost, stream), "D2H");
+    check(cudaMemsetAsync(a.ev_count, 0, sizeof(unsigned long long), stream), "memset");
+    check(cudaStreamSynchronize(stream), "events");
+    sink.fn(reinterpret_cast<const pp_step_event*>(ev_host), ne, sink.user);
+    n_events += ne;
+  };
+
   uint64_t trips = 0, launches = 0, compactions = 0;
   float kms[3] = {0, 0, 0};
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
-  // pinned mailbox: [0] busy slots after the last control kernel, [1] start counter
-  unsigned long long* mbox = nullptr;
-  check(cudaMallocHost(&mbox, 2 * sizeof(unsigned long long)), "cudaMallocHost");
   a.n_active = S;
   a.tmem_cols = tmem_cols;
   {
@@ -497,10 +679,8 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     bool coop = (env_size("PP200_FORCE_COOP", 0) != 0 || (tail_slots > 0 && count <= tail_slots)) && ewpb >= 1 &&
                 lwpb >= 1;
     if (ewpb >= 1 && lwpb >= 1) {
-      check(cudaFuncSetAttribute(var->eval_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(ewpb * ecoop_warp)), "cudaFuncSetAttribute");
-      check(cudaFuncSetAttribute(lsq_coop_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(lwpb * lcoop_warp)), "cudaFuncSetAttribute");
+      ensure_smem(var->eval_coop, ewpb * ecoop_warp, device);
+      ensure_smem(lsq_coop_fn, lwpb * lcoop_warp, device);
     }
     // one trip = control (step control, prediction, finalize, refill) followed by the heavy
     // operation of every busy slot.  Thread-per-path mode fuses the control into the evaluation
@@ -509,27 +689,27 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     // (instrumented mode) the three phases are bracketed: ev[0] ctrl ev[1] eval ev[2] lsq ev[3].
     auto launch_trip = [&](unsigned* busy_ptr, cudaEvent_t* ev) {
       void* args[] = {&a, &busy_ptr};
-      if (ev) cudaEventRecord(ev[0], stream);
+      if (ev) check(cudaEventRecord(ev[0], stream), "event");
       if (coop) {
         check(cudaLaunchKernel(var->step_trip, grid, blk, args, 0, stream), "launch step_trip");
-        if (ev) cudaEventRecord(ev[1], stream);
+        if (ev) check(cudaEventRecord(ev[1], stream), "event");
         const unsigned eb = static_cast<unsigned>((a.n_active + ewpb - 1) / ewpb);
         const unsigned lb = static_cast<unsigned>((a.n_active + lwpb - 1) / lwpb);
         check(cudaLaunchKernel(var->eval_coop, dim3(eb), dim3(32 * ewpb), targs, ewpb * ecoop_warp, stream),
               "launch eval_coop");
-        if (ev) cudaEventRecord(ev[2], stream);
+        if (ev) check(cudaEventRecord(ev[2], stream), "event");
         check(cudaLaunchKernel(lsq_coop_fn, dim3(lb), dim3(32 * lwpb), targs, lwpb * lcoop_warp, stream),
               "launch lsq_coop");
       } else {
-        if (ev) cudaEventRecord(ev[1], stream);
+        if (ev) check(cudaEventRecord(ev[1], stream), "event");
         check(cudaLaunchKernel(ctrl_eval_fn, egrid(), dim3(eblock), args, eval_smem, stream),
               "launch ctrl_eval_trip");
-        if (ev) cudaEventRecord(ev[2], stream);
+        if (ev) check(cudaEventRecord(ev[2], stream), "event");
         check(cudaLaunchKernel(lsq_fn, dim3(static_cast<unsigned>((a.n_active + lblock - 1) / lblock)), dim3(lblock), targs,
                                lsq_smem, stream),
               "launch lsq_trip");
       }
-      if (ev) cudaEventRecord(ev[3], stream);
+      if (ev) check(cudaEventRecord(ev[3], stream), "event");
       launches += coop ? 3 : 2;
     };
 
@@ -538,8 +718,6 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     const bool compact = env_size("PP200_COMPACT", 1) != 0;
     // compact when at most this fraction of the launched slots is busy (PP200_COMPACT_PCT)
     const double compact_frac = static_cast<double>(std::min<size_t>(99, env_size("PP200_COMPACT_PCT", 95))) / 100.0;
-    unsigned* holes = nullptr;
-    if (compact) check(cudaMallocAsync(reinterpret_cast<void**>(&holes), (2 * S + 2) * sizeof(unsigned), stream), "alloc");
     auto maybe_compact = [&](unsigned long long nbusy, unsigned long long started) -> bool {
       if (!compact || started < count || nbusy == 0 ||
           static_cast<double>(nbusy) > compact_frac * static_cast<double>(a.n_active))
@@ -572,12 +750,12 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
 
     if (env_size("PP200_KERNEL_TIMING", 0) != 0) {
       // instrumented mode: plain launches bracketed by events, per-kernel device time accumulated
-      cudaEvent_t ev[4];
-      for (auto& e : ev) cudaEventCreate(&e);
+      cudaEvent_t* ev = cx.kev;
       // PP200_TRIP_LOG=<file>: one line per trip (trip, busy slots, eval/lsq/control ms, launched
       // slots, tail mode)
       const char* log_path = std::getenv("PP200_TRIP_LOG");
-      FILE* trip_log = (log_path && *log_path) ? std::fopen(log_path, "a") : nullptr;
+      std::unique_ptr<FILE, int (*)(FILE*)> trip_log((log_path && *log_path) ? std::fopen(log_path, "a") : nullptr,
+                                                     [](FILE* f) { return f ? std::fclose(f) : 0; });
       for (;;) {
         check(cudaMemsetAsync(busy, 0, sizeof(unsigned), stream), "memset busy");
         const size_t trip_active = a.n_active;
@@ -588,70 +766,51 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
         check(cudaStreamSynchronize(stream), "tracker trip");
         const unsigned long long nbusy = *reinterpret_cast<unsigned*>(mbox);
         float tms[3] = {0, 0, 0};  // ctrl, eval (thread mode: control + evaluation), lsq
-        for (int k = 0; k < 3; ++k) cudaEventElapsedTime(&tms[k], ev[k], ev[k + 1]);
+        for (int k = 0; k < 3; ++k) check(cudaEventElapsedTime(&tms[k], ev[k], ev[k + 1]), "event time");
         kms[0] += tms[1];
         kms[1] += tms[2];
         kms[2] += tms[0];
         if (trip_log)
-          std::fprintf(trip_log, "%llu %llu %.4f %.4f %.4f %llu %d\n", static_cast<unsigned long long>(trips), nbusy,
+          std::fprintf(trip_log.get(), "%llu %llu %.4f %.4f %.4f %llu %d\n", static_cast<unsigned long long>(trips), nbusy,
                        tms[1], tms[2], tms[0], static_cast<unsigned long long>(trip_active), trip_coop ? 1 : 0);
         ++trips;
+        drain_events();
         if (nbusy == 0) break;
         maybe_compact(nbusy, mbox[1]);
       }
-      for (auto& e : ev) cudaEventDestroy(e);
-      if (trip_log) std::fclose(trip_log);
     } else {
       // one trip = evaluate, solve, control; trips are captured G at a time into a CUDA graph
       // whose last control kernel reports how many slots are still busy.  The graph is
       // re-captured when compaction shrinks the launch.
       auto capture = [&]() {
-        if (exec) cudaGraphExecDestroy(exec);
-        if (graph) cudaGraphDestroy(graph);
-        exec = nullptr;
-        graph = nullptr;
+        gh.reset();
         check(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "capture");
+        capg.active = true;
         check(cudaMemsetAsync(busy, 0, graph_trips * sizeof(unsigned), stream), "memset busy");
         for (size_t j = 0; j < graph_trips; ++j) launch_trip(busy + j, nullptr);
         launches -= (coop ? 3 : 2) * graph_trips;  // counted per graph launch below
-        check(cudaStreamEndCapture(stream, &graph), "end capture");
-        if (l2_persist && prop.persistingL2CacheMaxSize > 0) {
-          // make sure every captured kernel carries the stream's L2 access policy
-          cudaStreamAttrValue sattr{};
-          check(cudaStreamGetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &sattr), "get attr");
-          size_t nn = 0;
-          check(cudaGraphGetNodes(graph, nullptr, &nn), "graph nodes");
-          std::vector<cudaGraphNode_t> nodes(nn);
-          check(cudaGraphGetNodes(graph, nodes.data(), &nn), "graph nodes");
-          for (cudaGraphNode_t nd : nodes) {
-            cudaGraphNodeType ty;
-            check(cudaGraphNodeGetType(nd, &ty), "node type");
-            if (ty != cudaGraphNodeTypeKernel) continue;
-            cudaKernelNodeAttrValue kv{};
-            kv.accessPolicyWindow = sattr.accessPolicyWindow;
-            check(cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributeAccessPolicyWindow, &kv), "node attr");
-          }
-        }
-        check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
+        capg.active = false;
+        check(cudaStreamEndCapture(stream, &gh.graph), "end capture");
+        check(cudaGraphInstantiate(&gh.exec, gh.graph, 0), "graph instantiate");
       };
       capture();
       for (;;) {
-        check(cudaGraphLaunch(exec, stream), "graph launch");
+        check(cudaGraphLaunch(gh.exec, stream), "graph launch");
         check(cudaMemcpyAsync(mbox, busy + graph_trips - 1, sizeof(unsigned), cudaMemcpyDeviceToHost, stream), "D2H");
         check(cudaMemcpyAsync(mbox + 1, a.next, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream), "D2H");
         check(cudaStreamSynchronize(stream), "tracker trips");
         trips += graph_trips;
         launches += (coop ? 3 : 2) * graph_trips;
         const unsigned long long nbusy = *reinterpret_cast<unsigned*>(mbox);
+        drain_events();
         if (nbusy == 0) break;
         if (maybe_compact(nbusy, mbox[1])) capture();
       }
     }
-    if (holes) cudaFreeAsync(holes, stream);
   }
   unsigned long long work[2] = {0, 0};
   check(cudaMemcpyAsync(work, a.work, sizeof work, cudaMemcpyDeviceToHost, stream), "D2H");
-  cudaEventRecord(e2, stream);
+  check(cudaEventRecord(e[2], stream), "event");
 
   // records back to the caller's host buffers
   std::vector<double> div(count * 4);
@@ -668,28 +827,20 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   down(out->rejections, a.rec_rej, count * 4);
   down(div.data(), a.rec_div, count * 4 * sizeof(double));
   down(divflag.data(), a.rec_divflag, count);
-  cudaEventRecord(e3, stream);
-  for (void* p : temps) cudaFreeAsync(p, stream);
+  check(cudaEventRecord(e[3], stream), "event");
+  temps.release();
   check(cudaStreamSynchronize(stream), "record download");
   float ms_h2d = 0, ms_k = 0, ms_d2h = 0;
-  cudaEventElapsedTime(&ms_h2d, e0, e1);
-  cudaEventElapsedTime(&ms_k, e1, e2);
-  cudaEventElapsedTime(&ms_d2h, e2, e3);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  cudaEventDestroy(e2);
-  cudaEventDestroy(e3);
-  if (exec) cudaGraphExecDestroy(exec);
-  if (graph) cudaGraphDestroy(graph);
-  cudaFreeHost(mbox);
-  if (l2_persist && prop.persistingL2CacheMaxSize > 0) cudaCtxResetPersistingL2Cache();
-  cudaStreamDestroy(stream);
+  check(cudaEventElapsedTime(&ms_h2d, e[0], e[1]), "event time");
+  check(cudaEventElapsedTime(&ms_k, e[1], e[2]), "event time");
+  check(cudaEventElapsedTime(&ms_d2h, e[2], e[3]), "event time");
 
   // terminal divergence classification: m_est = log(growth) / log(shrink) with the host libm
-  // (tracker.cpp:429-431)
+  // (tracker.cpp:429-431); path ids of the shard's records
+  const uint64_t blk = a.shard_block;
   uint64_t newton_sum = 0;
   for (uint64_t i = 0; i < count; ++i) {
-    out->path_id[i] = lo + i;
+    out->path_id[i] = lo + ((i / blk) * a.shard_n + a.shard_r) * blk + i % blk;
     newton_sum += out->newton_iters[i];
     if (!divflag[i]) continue;
     const double first = div[i * 4 + 0], last = div[i * 4 + 1], uf = div[i * 4 + 2], ul = div[i * 4 + 3];
@@ -714,15 +865,24 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     stats->eval_ms = kms[0];
     stats->lsq_ms = kms[1];
     stats->step_ms = kms[2];
+    stats->events = n_events;
     stats->wall_ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
   }
+  (void)compactions;
 }
 
 // ---------------------------------------------------------------------------------------------
 // kernel-level parity entry points (host <-> planar transposition happens here)
 // ---------------------------------------------------------------------------------------------
 namespace {
+// the planar accessors form offsets in 32 bits (track_impl.cuh, Planar::at): every planar array of
+// a kernel-level call must hold fewer than 2^32 doubles (callers chunk larger batches)
+void check_planar_size(size_t doubles, const char* what) {
+  if (doubles >= (static_cast<size_t>(1) << 32))
+    throw InvalidArgument(std::string(what) + ": batch too large (a planar array would exceed 2^32 doubles)");
+}
+
 // user layout [item][elem][2L]  <->  planar [elem][plane][item]
 void to_planar(const double* src, double* dst, size_t items, size_t elems, size_t w) {
   for (size_t i = 0; i < items; ++i)
@@ -743,34 +903,31 @@ void device_eval(const Plan& plan, DevicePlan* dp, uint32_t batch, const double*
   const uint32_t n = plan.dim, np = plan.n_polys, L = plan.L, w = 2 * L;
   const dev::Variant* var = pick_variant(plan.prec, n, plan.max_k);
   if (var == nullptr) throw InvalidArgument("system beyond the compiled kernels");
+  check_planar_size(static_cast<size_t>(np) * n * w * batch, "pp_eval_batch");
   std::vector<double> xp(static_cast<size_t>(batch) * n * w), tp(static_cast<size_t>(batch) * L);
   to_planar(points, xp.data(), batch, n, w);
   to_planar(t, tp.data(), batch, 1, L);
-  double* dx = upload(xp);
-  double* dt = upload(tp);
-  double* ds = dmalloc<double>(static_cast<size_t>(batch) * np * w);
-  double* dj = dmalloc<double>(static_cast<size_t>(batch) * np * n * w);
+  DevBuf<double> dx(xp);
+  DevBuf<double> dt(tp);
+  DevBuf<double> ds(static_cast<size_t>(batch) * np * w);
+  DevBuf<double> dj(static_cast<size_t>(batch) * np * n * w);
   dev::EvalArgs a{};
   a.plan = plan_args(plan, dp);
   a.batch = batch;
-  a.x = dx;
-  a.t = dt;
-  a.sys = ds;
-  a.jac = dj;
+  a.x = dx.p;
+  a.t = dt.p;
+  a.sys = ds.p;
+  a.jac = dj.p;
   int block = 128;
   while (block > 32 && static_cast<size_t>(block) * 2 * n * w * sizeof(double) > 200 * 1024) block /= 2;
   const size_t smem = static_cast<size_t>(block) * 2 * n * w * sizeof(double);
-  check(cudaFuncSetAttribute(var->eval, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)), "attr");
+  ensure_smem(var->eval, smem, device);
   void* args[] = {&a};
   check(cudaLaunchKernel(var->eval, dim3((batch + block - 1) / block), dim3(block), args, smem, 0), "launch eval");
   check(cudaDeviceSynchronize(), "eval kernel");
   std::vector<double> hs(static_cast<size_t>(batch) * np * w), hj(static_cast<size_t>(batch) * np * n * w);
-  check(cudaMemcpy(hs.data(), ds, hs.size() * 8, cudaMemcpyDeviceToHost), "D2H");
-  check(cudaMemcpy(hj.data(), dj, hj.size() * 8, cudaMemcpyDeviceToHost), "D2H");
-  cudaFree(dx);
-  cudaFree(dt);
-  cudaFree(ds);
-  cudaFree(dj);
+  check(cudaMemcpy(hs.data(), ds.p, hs.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+  check(cudaMemcpy(hj.data(), dj.p, hj.size() * 8, cudaMemcpyDeviceToHost), "D2H");
   from_planar(hs.data(), sys, batch, np, w);
   if (jac) {
     // planar element v*np + p  ->  user row p*n + v
@@ -792,82 +949,82 @@ double device_bench_eval(const Plan& plan, DevicePlan* dp, uint32_t batch, const
   const uint32_t n = plan.dim, np = plan.n_polys, L = plan.L, w = 2 * L;
   const dev::Variant* var = pick_variant(plan.prec, n, plan.max_k);
   if (var == nullptr) throw InvalidArgument("system beyond the compiled kernels");
+  check_planar_size(static_cast<size_t>(np) * n * w * batch, "pp_bench_eval");
   std::vector<double> xv(xp, xp + static_cast<size_t>(batch) * n * w), tv(tp, tp + static_cast<size_t>(batch) * L);
-  double* dx = upload(xv);
-  double* dt = upload(tv);
-  double* ds = dmalloc<double>(static_cast<size_t>(batch) * np * w);
-  double* dj = dmalloc<double>(static_cast<size_t>(batch) * np * n * w);
+  DevBuf<double> dx(xv);
+  DevBuf<double> dt(tv);
+  DevBuf<double> ds(static_cast<size_t>(batch) * np * w);
+  DevBuf<double> dj(static_cast<size_t>(batch) * np * n * w);
   dev::EvalArgs a{};
   a.plan = plan_args(plan, dp);
   a.batch = batch;
-  a.x = dx;
-  a.t = dt;
-  a.sys = ds;
-  a.jac = dj;
+  a.x = dx.p;
+  a.t = dt.p;
+  a.sys = ds.p;
+  a.jac = dj.p;
   int block = 128;
   while (block > 32 && static_cast<size_t>(block) * 2 * n * w * sizeof(double) > 200 * 1024) block /= 2;
   const size_t smem = static_cast<size_t>(block) * 2 * n * w * sizeof(double);
-  check(cudaFuncSetAttribute(var->eval, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)), "attr");
+  ensure_smem(var->eval, smem, device);
   void* args[] = {&a};
   const dim3 grid((batch + block - 1) / block);
   check(cudaLaunchKernel(var->eval, grid, dim3(block), args, smem, 0), "launch eval");  // warm-up
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
-  cudaEventRecord(e0, 0);
+  EvPair ev;
+  check(cudaEventRecord(ev.e0, 0), "event");
   for (uint32_t r = 0; r < std::max<uint32_t>(reps, 1); ++r)
     check(cudaLaunchKernel(var->eval, grid, dim3(block), args, smem, 0), "launch eval");
-  cudaEventRecord(e1, 0);
-  check(cudaEventSynchronize(e1), "eval kernel");
+  check(cudaEventRecord(ev.e1, 0), "event");
+  check(cudaEventSynchronize(ev.e1), "eval kernel");
   float ms = 0;
-  cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
+  check(cudaEventElapsedTime(&ms, ev.e0, ev.e1), "event time");
   // eval_kernel returns H (not -H) in sys
-  check(cudaMemcpy(sys, ds, static_cast<size_t>(batch) * np * w * 8, cudaMemcpyDeviceToHost), "D2H");
+  check(cudaMemcpy(sys, ds.p, static_cast<size_t>(batch) * np * w * 8, cudaMemcpyDeviceToHost), "D2H");
   std::vector<double> hj(static_cast<size_t>(batch) * np * n * w);
-  check(cudaMemcpy(hj.data(), dj, hj.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+  check(cudaMemcpy(hj.data(), dj.p, hj.size() * 8, cudaMemcpyDeviceToHost), "D2H");
   for (size_t p = 0; p < np; ++p)
     for (size_t v = 0; v < n; ++v)
       std::memcpy(jac + (p * n + v) * w * batch, hj.data() + (v * np + p) * w * batch, w * batch * sizeof(double));
-  cudaFree(dx);
-  cudaFree(dt);
-  cudaFree(ds);
-  cudaFree(dj);
   return ms / std::max<uint32_t>(reps, 1);
 }
 
-void device_lsq(int prec, uint32_t n, uint32_t batch, const double* a, const double* b, double* x,
-                uint8_t* ok, int device) {
+void device_lsq(int prec, uint32_t m, uint32_t n, uint32_t batch, const double* a, const double* b, double* x,
+                uint8_t* ok, double* q_out, double* r_out, int device) {
   if (batch == 0) return;
   DeviceGuard g(device);
   const uint32_t L = prec == 0 ? 1 : (prec == 1 ? 2 : 4), w = 2 * L;
-  const dev::Variant* var = pick_variant(prec, n, 2);
+  const dev::Variant* var = pick_variant(prec, std::max(m, n), 2);
   if (var == nullptr) throw InvalidArgument("least-squares size beyond the compiled kernels");
-  std::vector<double> ap(static_cast<size_t>(batch) * n * n * w), bp(static_cast<size_t>(batch) * n * w);
-  to_planar(a, ap.data(), batch, static_cast<size_t>(n) * n, w);
-  to_planar(b, bp.data(), batch, n, w);
-  double* da = upload(ap);
-  double* db = upload(bp);
-  double* dr = dmalloc<double>(static_cast<size_t>(batch) * n * (n + 1) / 2 * w);
-  double* dy = dmalloc<double>(static_cast<size_t>(batch) * n * w);
-  double* dxv = dmalloc<double>(static_cast<size_t>(batch) * n * w);
-  uint8_t* dok = dmalloc<uint8_t>(batch);
-  dev::LsqArgs args{static_cast<int>(n), batch, default_rank_tol(prec), da, dr, db, dy, dxv, dok};
+  check_planar_size(static_cast<size_t>(m) * n * w * batch, "pp_lsq_batch");
+  const size_t nr = static_cast<size_t>(n) * (n + 1) / 2;
+  std::vector<double> ap(static_cast<size_t>(batch) * m * n * w), bp(static_cast<size_t>(batch) * m * w);
+  to_planar(a, ap.data(), batch, static_cast<size_t>(m) * n, w);
+  to_planar(b, bp.data(), batch, m, w);
+  DevBuf<double> da(ap), db(bp), dr(static_cast<size_t>(batch) * nr * w), dy(static_cast<size_t>(batch) * n * w),
+      dxv(static_cast<size_t>(batch) * n * w);
+  DevBuf<uint8_t> dok(batch);
+  dev::LsqArgs args{static_cast<int>(n), static_cast<int>(m), batch, default_rank_tol(prec), da.p, dr.p, db.p, dy.p,
+                    dxv.p, dok.p};
   void* pa[] = {&args};
   int block = 128;
-  while (block > 32 && static_cast<size_t>(block) * n * w * sizeof(double) > 200 * 1024) block /= 2;
-  const size_t smem = static_cast<size_t>(block) * n * w * sizeof(double);
-  check(cudaFuncSetAttribute(var->lsq, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)), "attr");
+  while (block > 32 && static_cast<size_t>(block) * m * w * sizeof(double) > 200 * 1024) block /= 2;
+  const size_t smem = static_cast<size_t>(block) * m * w * sizeof(double);
+  ensure_smem(var->lsq, smem, device);
   check(cudaLaunchKernel(var->lsq, dim3((batch + block - 1) / block), dim3(block), pa, smem, 0), "launch lsq");
   check(cudaDeviceSynchronize(), "lsq kernel");
   std::vector<double> hx(static_cast<size_t>(batch) * n * w);
-  check(cudaMemcpy(hx.data(), dxv, hx.size() * 8, cudaMemcpyDeviceToHost), "D2H");
-  check(cudaMemcpy(ok, dok, batch, cudaMemcpyDeviceToHost), "D2H");
-  for (void* p : {static_cast<void*>(da), static_cast<void*>(db), static_cast<void*>(dr),
-                  static_cast<void*>(dy), static_cast<void*>(dxv), static_cast<void*>(dok)})
-    cudaFree(p);
+  check(cudaMemcpy(hx.data(), dxv.p, hx.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+  check(cudaMemcpy(ok, dok.p, batch, cudaMemcpyDeviceToHost), "D2H");
   from_planar(hx.data(), x, batch, n, w);
+  if (q_out) {  // Q, column-major m x n per system
+    std::vector<double> hq(ap.size());
+    check(cudaMemcpy(hq.data(), da.p, hq.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+    from_planar(hq.data(), q_out, batch, static_cast<size_t>(m) * n, w);
+  }
+  if (r_out) {  // R, packed upper triangle: (row j, column i >= j) at j + i(i+1)/2
+    std::vector<double> hr(static_cast<size_t>(batch) * nr * w);
+    check(cudaMemcpy(hr.data(), dr.p, hr.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+    from_planar(hr.data(), r_out, batch, nr, w);
+  }
 }
 
 }  // namespace pp

@@ -18,9 +18,22 @@ struct DevicePlan;
 DevicePlan* device_plan_upload(const Plan& plan, int device);
 void device_plan_free(DevicePlan* dp);
 
-// track_all on the device: starts [lo, hi) -> records (host buffers in `out`).
+// block-cyclic shard of a start range (pp_shard); count == 1 is the whole range
+struct TrackShard {
+  uint64_t index = 0, count = 1, block = 1;
+};
+uint64_t shard_size(uint64_t lo, uint64_t hi, const TrackShard& sh);
+
+// step-event sink (ProgressSink); fn == nullptr disables events
+struct EventSink {
+  pp_event_sink fn = nullptr;
+  void* user = nullptr;
+};
+
+// track_all on the device: the shard's starts of [lo, hi) -> records (host buffers in `out`).
 void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_track_config& cfg,
-                  uint64_t lo, uint64_t hi, int device, pp_records* out, pp_run_stats* stats);
+                  uint64_t lo, uint64_t hi, const TrackShard& shard, const EventSink& sink, int device,
+                  pp_records* out, pp_run_stats* stats);
 
 // eval_system_batch on the device (host buffers, layouts of pp_eval_batch)
 void device_eval(const Plan& plan, DevicePlan* dp, uint32_t batch, const double* points,
@@ -30,15 +43,18 @@ void device_eval(const Plan& plan, DevicePlan* dp, uint32_t batch, const double*
 double device_bench_eval(const Plan& plan, DevicePlan* dp, uint32_t batch, const double* xp, const double* tp,
                          uint32_t reps, double* sys, double* jac, int device);
 
-// batched least_squares_solve (layouts of pp_lsq_batch)
-void device_lsq(int prec, uint32_t n, uint32_t batch, const double* a, const double* b, double* x,
-                uint8_t* ok, int device);
+// batched least_squares_solve / mgs_qr for m x n systems (layouts of pp_lsq_batch_mn)
+void device_lsq(int prec, uint32_t m, uint32_t n, uint32_t batch, const double* a, const double* b, double* x,
+                uint8_t* ok, double* q_out, double* r_out, int device);
 
 // rank tolerance of the reference's least_squares_solve default (linalg.hpp:44-52)
 inline double default_rank_tol(int prec) { return prec == 0 ? 1e-8 : (prec == 1 ? 1e-16 : 1e-32); }
 
 // largest dimension / monomial support the compiled kernels cover
 bool device_supports(uint32_t n, uint32_t max_k);
+
+// CUDA devices visible (0 without a usable driver)
+int device_count();
 
 // measured FP64 pipe operations per second (DFMA microbenchmark)
 double device_fp64_peak(int device);

@@ -16,6 +16,18 @@ constexpr int kHistDepth = 5;  // predictor history depth (reference tracker.cpp
 // slot-state field counts (enums F_*, R_*, D_* in track_impl.cuh)
 constexpr int kIntFields = 14, kRealFields = 4, kDblFields = 3;
 
+// StepEvent (tracker.hpp:62-69) as written by the device; layout-identical to pp_step_event
+struct StepEventRec {
+  unsigned long long path_id;
+  double t;
+  double h;
+  uint32_t newton_iters;
+  int8_t status;
+  uint8_t accepted;
+  uint8_t pad[2];
+};
+static_assert(sizeof(StepEventRec) == 32, "event record layout");
+
 // Plan tables, device pointers (layouts documented in host.hpp, struct Plan)
 struct PlanArgs {
   const int32_t* term_info;  // 4 per term
@@ -45,8 +57,12 @@ struct TrackArgs {
   double rtol, utol, h_init, h_min, h_max, expand, contract, div_bound, rank_tol;
   int max_newton, expand_after;
   uint32_t max_steps;
-  // start-index range and refill counter
-  unsigned long long lo, hi;
+  // start-index range and refill counter.  The slot that draws refill number k (k < count) tracks
+  // start index lo + ((k / shard_block) * shard_n + shard_r) * shard_block + k % shard_block: the
+  // identity when shard_n == 1, else shard shard_r of a block-cyclic partition of [lo, hi)
+  // among shard_n shards (multi-GPU load balance); its record is record k.
+  unsigned long long lo, hi, count;
+  unsigned long long shard_block, shard_n, shard_r;
   unsigned long long* next;
   unsigned long long* work;  // [0] evaluations, [1] least-squares solves issued
   // per-slot storage (S slots).  Planar arrays: element e, limb-plane p, slot s at ((e*P)+p)*S+s.
@@ -66,6 +82,11 @@ struct TrackArgs {
   uint32_t *rec_steps, *rec_newton, *rec_rej;
   double* rec_div;     // [rec][4]: first, last, u_first, u_last of the terminal-divergence test
   uint8_t* rec_divflag;
+  // step events (ProgressSink, tracker.hpp:62-70): one per step-control decision, appended at an
+  // atomic cursor; ev == nullptr disables them.  Drained by the host after every graph launch.
+  StepEventRec* ev;
+  unsigned long long* ev_count;
+  unsigned long long ev_cap;
 };
 
 // eval_system_batch for independent points (one thread per point)
@@ -81,11 +102,12 @@ struct EvalArgs {
 // least_squares_solve for independent systems (one thread per system)
 struct LsqArgs {
   int n;
+  int m;       // rows (m >= n)
   uint32_t batch;
   double rank_tol;
-  double* a;   // planar, element col*n + row (overwritten by Q)
+  double* a;   // planar, element col*m + row (overwritten by Q)
   double* r;   // planar, packed upper triangle, n(n+1)/2
-  double* b;   // planar, element row
+  double* b;   // planar, element row (m)
   double* y;   // planar scratch, n
   double* x;   // planar out, n
   uint8_t* ok;
@@ -122,6 +144,16 @@ struct MoveArgs {
   unsigned* counts;     // [0] holes, [1] movers
 };
 void launch_compaction(const MoveArgs& m, void* stream);
+
+// register-resident least-squares solvers, compiled for a few dimensions N (track_impl.cuh
+// lsq_trip_reg): `stream` re-reads q_i for its axpy, `hold` keeps it in registers
+struct LsqReg {
+  int n;
+  const void* stream;  // __global__ void(TrackArgs)
+  const void* hold;    // __global__ void(TrackArgs)
+};
+const LsqReg* lsq_reg_d(int* count);
+const LsqReg* lsq_reg_dd(int* count);
 
 const Variant* variants_d(int* count);
 const Variant* variants_dd(int* count);

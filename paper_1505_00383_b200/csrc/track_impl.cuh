@@ -539,14 +539,15 @@ __device__ __forceinline__ void prefetch_column(const GA& Q, int col, int n, siz
 }
 
 template <class R, class GA, class CA, bool kUniform>
-__device__ bool lsq_solve_c(int n, double rank_tol, const GA& Q, const GA& Rm, const GA& B, const GA& Y,
+__device__ bool lsq_solve_c(int n, int m, double rank_tol, const GA& Q, const GA& Rm, const GA& B, const GA& Y,
                             size_t s, const CA& C) {
+  // m x n (m >= n rows; the tracker's systems are square, m == n): Q column-major, element col*m + row
   const cx<R> zero = czero<R>();
   R max_norm = rfrom<R>(0.0);
   for (int j = 0; j < n; ++j) {
     R acc = rfrom<R>(0.0);
 PP_UNROLL_ROWS
-    for (int r = 0; r < n; ++r) acc = radd(acc, cabs2(Q.ld(j * n + r, s)));
+    for (int r = 0; r < m; ++r) acc = radd(acc, cabs2(Q.ld(j * m + r, s)));
     const R nj = rsqrt(acc);
     if (rcmp(nj, max_norm) > 0) max_norm = nj;
   }
@@ -557,25 +558,25 @@ PP_UNROLL_ROWS
   bool ok = true;
   for (int k = 0; k < n; ++k) {
 PP_UNROLL_ROWS
-    for (int r = 0; r < n; ++r) C.st(r, Q.ld(k * n + r, s));
+    for (int r = 0; r < m; ++r) C.st(r, Q.ld(k * m + r, s));
     const int rk = k * (k + 1) / 2;
     for (int pass = 0; pass < 2; ++pass) {
       for (int i = 0; i < k; ++i) {
         // next column read: q_(i+1), else q_0 of the second pass, else the next column
         const int nxt = i + 1 < k ? i + 1 : (pass == 0 ? 0 : k + 1);
-        if (nxt < n) prefetch_column<R>(Q, nxt, n, s);
+        if (nxt < n) prefetch_column<R>(Q, nxt, m, s);
         cx<R> rik = zero;
 PP_UNROLL_ROWS
-        for (int r = 0; r < n; ++r) rik = cadd(rik, cmul(cconj(Q.ld(i * n + r, s)), C.ld(r)));
+        for (int r = 0; r < m; ++r) rik = cadd(rik, cmul(cconj(Q.ld(i * m + r, s)), C.ld(r)));
         const cx<R> prev = pass == 0 ? zero : Rm.ld(i + rk, s);
         Rm.st(i + rk, s, cadd(prev, rik));
 PP_UNROLL_ROWS
-        for (int r = 0; r < n; ++r) C.st(r, csub(C.ld(r), cmul(rik, Q.ld(i * n + r, s))));
+        for (int r = 0; r < m; ++r) C.st(r, csub(C.ld(r), cmul(rik, Q.ld(i * m + r, s))));
       }
     }
     R acc = rfrom<R>(0.0);
 PP_UNROLL_ROWS
-    for (int r = 0; r < n; ++r) acc = radd(acc, cabs2(C.ld(r)));
+    for (int r = 0; r < m; ++r) acc = radd(acc, cabs2(C.ld(r)));
     const R rkk = rsqrt(acc);
     if (rcmp(rkk, tol) <= 0) {
       if (!kUniform) return false;
@@ -585,9 +586,9 @@ PP_UNROLL_ROWS
     const R rinv = rdiv(rfrom<R>(1.0), rkk);
     cx<R> y = zero;
 PP_UNROLL_ROWS
-    for (int r = 0; r < n; ++r) {
+    for (int r = 0; r < m; ++r) {
       const cx<R> q = cmulr(C.ld(r), rinv);
-      Q.st(k * n + r, s, q);
+      Q.st(k * m + r, s, q);
       y = cadd(y, cmul(cconj(q), B.ld(r, s)));  // y_k = <q_k, b> (linalg.hpp:117)
     }
     Y.st(k, s, y);
@@ -663,7 +664,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) lsq_trip(const TrackArgs
   if (!kTmem) {
     if (!need) return;
     const SmemRow<R> C{Planar<R>{smem, blockDim.x}, threadIdx.x};
-    const bool ok = lsq_solve_c<R, decltype(J), SmemRow<R>, false>(n, a.rank_tol, J, Rm, B, Y, s, C);
+    const bool ok = lsq_solve_c<R, decltype(J), SmemRow<R>, false>(n, n, a.rank_tol, J, Rm, B, Y, s, C);
     si(F_OK, s) = ok ? 1 : 0;
     if (!ok) return;
     // x += dx; update and iterate norms (tracker.cpp:258-264)
@@ -684,7 +685,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) lsq_trip(const TrackArgs
     const int warp = threadIdx.x >> 5;
     const TmemRow<R> C{base + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + static_cast<uint32_t>((warp >> 2) * n * 4 * L)};
     if (__any_sync(0xffffffffu, need)) {
-      const bool ok = lsq_solve_c<R, decltype(J), TmemRow<R>, true>(n, a.rank_tol, J, Rm, B, Y, s, C);
+      const bool ok = lsq_solve_c<R, decltype(J), TmemRow<R>, true>(n, n, a.rank_tol, J, Rm, B, Y, s, C);
       if (need) si(F_OK, s) = ok ? 1 : 0;
       double dxn = 0.0, xn = 0.0;
       for (int v = 0; v < n; ++v) {
@@ -707,6 +708,118 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) lsq_trip(const TrackArgs
 }
 
 // ---------------------------------------------------------------------------------------------
+// least squares with a compile-time dimension N: the Gram-Schmidt column lives in registers
+// ---------------------------------------------------------------------------------------------
+// The same operation sequence as lsq_solve_c (linalg.hpp:79-125), with every row loop unrolled so
+// the column C is register-resident.  No shared memory is used, so the whole L1 caches the
+// solver's Q/R columns.  kHoldQ additionally keeps the projected column q_i in registers (QB)
+// from its dot product to its axpy, and refills QB row by row with the next column to be
+// projected while the axpy consumes it (software pipelining: the load of row r is issued as soon
+// as row r of q_i is dead), so every q_i is read once per projection instead of twice.
+template <class R, int N, bool kHoldQ, class GA>
+__device__ __forceinline__ bool lsq_solve_reg(double rank_tol, const GA& Q, const GA& Rm, const GA& B,
+                                              const GA& Y, size_t s, cx<R> (&C)[N]) {
+  const cx<R> zero = czero<R>();
+  R max_norm = rfrom<R>(0.0);
+#pragma unroll 1
+  for (int j = 0; j < N; ++j) {
+    R acc = rfrom<R>(0.0);
+#pragma unroll
+    for (int r = 0; r < N; ++r) acc = radd(acc, cabs2(Q.ld(j * N + r, s)));
+    const R nj = rsqrt(acc);
+    if (rcmp(nj, max_norm) > 0) max_norm = nj;
+  }
+  const R tol = rmul(max_norm, rfrom<R>(rank_tol));
+
+  cx<R> QB[kHoldQ ? N : 1];
+#pragma unroll 1
+  for (int k = 0; k < N; ++k) {
+#pragma unroll
+    for (int r = 0; r < N; ++r) C[r] = Q.ld(k * N + r, s);
+    const int rk = k * (k + 1) / 2;
+    if (kHoldQ && k > 0) {
+#pragma unroll
+      for (int r = 0; r < N; ++r) QB[kHoldQ ? r : 0] = Q.ld(r, s);  // q_0
+    }
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll 1
+      for (int i = 0; i < k; ++i) {
+        cx<R> rik = zero;
+#pragma unroll
+        for (int r = 0; r < N; ++r)
+          rik = cadd(rik, cmul(cconj(kHoldQ ? QB[kHoldQ ? r : 0] : Q.ld(i * N + r, s)), C[r]));
+        const cx<R> prev = pass == 0 ? zero : Rm.ld(i + rk, s);
+        Rm.st(i + rk, s, cadd(prev, rik));
+        // the next column this thread projects on: q_(i+1), else q_0 of the second pass
+        const int nxt = i + 1 < k ? i + 1 : (pass == 0 ? 0 : -1);
+#pragma unroll
+        for (int r = 0; r < N; ++r) {
+          if (kHoldQ) {
+            C[r] = csub(C[r], cmul(rik, QB[kHoldQ ? r : 0]));
+            if (nxt >= 0) QB[kHoldQ ? r : 0] = Q.ld(nxt * N + r, s);
+          } else {
+            C[r] = csub(C[r], cmul(rik, Q.ld(i * N + r, s)));
+          }
+        }
+      }
+    }
+    R acc = rfrom<R>(0.0);
+#pragma unroll
+    for (int r = 0; r < N; ++r) acc = radd(acc, cabs2(C[r]));
+    const R rkk = rsqrt(acc);
+    if (rcmp(rkk, tol) <= 0) return false;
+    Rm.st(k + rk, s, cx<R>{rkk, rfrom<R>(0.0)});
+    const R rinv = rdiv(rfrom<R>(1.0), rkk);
+    cx<R> y = zero;
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      const cx<R> q = cmulr(C[r], rinv);
+      Q.st(k * N + r, s, q);
+      y = cadd(y, cmul(cconj(q), B.ld(r, s)));  // y_k = <q_k, b> (linalg.hpp:117)
+    }
+    Y.st(k, s, y);
+  }
+  // back substitution R x = y (linalg.hpp:118-122), unrolled so x stays in registers (C)
+#pragma unroll
+  for (int j = N - 1; j >= 0; --j) {
+    cx<R> acc = Y.ld(j, s);
+#pragma unroll
+    for (int i = j + 1; i < N; ++i) acc = csub(acc, cmul(Rm.ld(j + i * (i + 1) / 2, s), C[i]));
+    C[j] = cdiv(acc, Rm.ld(j + j * (j + 1) / 2, s));
+  }
+  return true;
+}
+
+template <class R, int N, bool kHoldQ, int kMinBlocks>
+__global__ void __launch_bounds__(128, kMinBlocks) lsq_trip_reg(const TrackArgs a) {
+  static_assert(PP_SLOT_TILED, "the register solver reads the slot-tiled solver arrays");
+  const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= a.n_active) return;
+  const SlotInts si{a.si, a.S};
+  const int mode = si(F_MODE, s);
+  if (mode != M_NEWTON && mode != M_REFINE) return;
+  const Tiled<R> J{a.J, static_cast<uint32_t>(N * N)}, Rm{a.Rm, static_cast<uint32_t>(N * (N + 1) / 2)},
+      B{a.B, static_cast<uint32_t>(N)}, Y{a.Y, static_cast<uint32_t>(N)};
+  cx<R> C[N];
+  const bool ok = lsq_solve_reg<R, N, kHoldQ>(a.rank_tol, J, Rm, B, Y, s, C);
+  si(F_OK, s) = ok ? 1 : 0;
+  if (!ok) return;
+  // x += dx; update and iterate norms (tracker.cpp:258-264)
+  const Planar<R> X{a.x, a.S};
+  double dxn = 0.0, xn = 0.0;
+#pragma unroll
+  for (int v = 0; v < N; ++v) {
+    const cx<R> xv = cadd(X.ld(v, s), C[v]);
+    X.st(v, s, xv);
+    dxn = f_max(dxn, cabsd(C[v]));
+    xn = f_max(xn, cabsd(xv));
+  }
+  a.sd[D_DXN * a.S + s] = dxn;
+  a.sd[D_XN * a.S + s] = xn;
+}
+
+// ---------------------------------------------------------------------------------------------
 // per-path control: corrector bookkeeping, step control, status, prediction, finalize and record
 // output, refill from the start counter.  Shared by the trip kernels (state in SoA global memory)
 // and the persistent kernel (state in registers).
@@ -726,6 +839,12 @@ struct HeavyOut {
   R resid_r;
   bool ok;
 };
+
+// record of start index `path` (inverse of the refill map)
+__device__ __forceinline__ size_t record_index(const TrackArgs& a, unsigned long long path) {
+  const unsigned long long off = path - a.lo, blk = a.shard_block;
+  return static_cast<size_t>(off / (blk * a.shard_n) * blk + off % blk);
+}
 
 // X: the slot's working point (xs = its column there); every other per-slot array is global at s
 template <class R>
@@ -815,6 +934,22 @@ __device__ __forceinline__ void control(const TrackArgs& a, SlotState<R>& st, co
         st.h = rmuld(st.h, a.contract);
         for (int v = 0; v < n; ++v) xacc_norm = f_max(xacc_norm, cabsd(XA.ld(v, s)));
       }
+      if (a.ev != nullptr) {
+        // the sink's StepEvent (tracker.cpp:312-315): t and h after the decision, this step's
+        // corrector iterations, and the status as it stands before this round's check
+        const unsigned long long e = atomicAdd(a.ev_count, 1ull);
+        if (e < a.ev_cap) {
+          StepEventRec r;
+          r.path_id = st.path;
+          r.t = rtod(st.t);
+          r.h = rtod(st.h);
+          r.newton_iters = static_cast<uint32_t>(st.it);
+          r.status = static_cast<int8_t>(st.status);
+          r.accepted = st.corrected ? 1 : 0;
+          r.pad[0] = r.pad[1] = 0;
+          a.ev[e] = r;
+        }
+      }
       // status on the accepted point (tracker.cpp:319-338)
       if (xacc_norm > a.div_bound) {
         st.status = ST_FAILED;
@@ -835,7 +970,7 @@ __device__ __forceinline__ void control(const TrackArgs& a, SlotState<R>& st, co
         st.corrected = 0;
         st.sing = 0;
       } else {
-        const size_t rec = static_cast<size_t>(st.path - a.lo);
+        const size_t rec = record_index(a, st.path);
         uint8_t flag = 0;
         if (st.status == ST_FAILED && st.reason != RS_DIVERGED && f_sub(1.0, rtod(st.t)) < 0.01 && st.len >= 3) {
           // terminal divergence test inputs (tracker.cpp:406-432); the log ratio is taken on
@@ -879,7 +1014,7 @@ __device__ __forceinline__ void control(const TrackArgs& a, SlotState<R>& st, co
     if (stop || st.rit >= 3) st.mode = M_FINAL;
   } else if (st.mode == M_FINAL) {
     // final residual ||f(xacc)|| at level R and the certificate (tracker.cpp:480-506)
-    const size_t rec = static_cast<size_t>(st.path - a.lo);
+    const size_t rec = record_index(a, st.path);
     int st_out = st.status, rs_out = st.reason;
     if (st_out == ST_SUCCESS && rtod(ho.resid_r) > f_mul(10.0, a.rtol)) {
       st_out = ST_FAILED;
@@ -898,10 +1033,12 @@ __device__ __forceinline__ void control(const TrackArgs& a, SlotState<R>& st, co
 
   if (st.mode == M_IDLE) {
     // refill: next start index; seed (tracker.cpp:135-153) and the first prediction
-    st.path = a.lo + atomicAdd(a.next, 1ull);
-    if (st.path >= a.hi) {
+    const unsigned long long k = atomicAdd(a.next, 1ull);
+    if (k >= a.count) {
       st.mode = M_DONE;
     } else {
+      const unsigned long long blk = a.shard_block;
+      st.path = a.lo + ((k / blk) * a.shard_n + a.shard_r) * blk + k % blk;
       if (a.total_degree) {
         unsigned long long rem = st.path;
         for (int i = n - 1; i >= 0; --i) {
@@ -1380,7 +1517,7 @@ __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
   if (s >= a.batch) return;
   const Planar<R> Q{a.a, a.batch}, Rm{a.r, a.batch}, B{a.b, a.batch}, Y{a.y, a.batch}, X{a.x, a.batch};
   const Planar<R> C{smem, blockDim.x};
-  const bool ok = lsq_solve_c<R, Planar<R>, SmemRow<R>, false>(a.n, a.rank_tol, Q, Rm, B, Y, s, SmemRow<R>{C, threadIdx.x});
+  const bool ok = lsq_solve_c<R, Planar<R>, SmemRow<R>, false>(a.n, a.m, a.rank_tol, Q, Rm, B, Y, s, SmemRow<R>{C, threadIdx.x});
   a.ok[s] = ok ? 1 : 0;
   for (int v = 0; v < a.n; ++v) X.st(v, s, ok ? C.ld(v, threadIdx.x) : czero<R>());
 }
@@ -1401,3 +1538,8 @@ __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
    reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, true>),                        \
    reinterpret_cast<const void*>(&pp::dev::ctrl_eval_trip<R, KM, true, (sizeof(R) < 32 ? 4 : 1)>),             \
    reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, true, 256, 2>)}
+
+// register-resident least-squares solvers of one level for dimension N
+#define PP_LSQ_REG(R, N)                                                                        \
+  {N, reinterpret_cast<const void*>(&pp::dev::lsq_trip_reg<R, N, false, 4>),                   \
+   reinterpret_cast<const void*>(&pp::dev::lsq_trip_reg<R, N, true, (sizeof(R) == 8 ? 4 : 2)>)}

@@ -1,6 +1,6 @@
 """The north-star job: every total-degree start path of cyclic 10-roots (3,628,800 paths) tracked to
 t = 1 in complex double-double on this GPU (or on one shard of [0, 3628800) per rank under
-torchrun), with the classification counts and the number of distinct converged endpoints.
+torchrun: block-cyclic shards, blocks of 64), with the classification counts and the number of distinct converged endpoints.
 cyclic-10 has 34,940 isolated solutions, which a complete run should find.
 
     python scripts/track_full.py [--lo 0 --hi 3628800] [--chunk 3628800]
@@ -29,9 +29,9 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     device = int(os.environ.get("LOCAL_RANK", "0"))
-    span = args.hi - args.lo
-    lo = args.lo + span * rank // world
-    hi = args.lo + span * (rank + 1) // world
+    # this rank's block-cyclic shard of [lo, hi) (pp_shard; blocks of 64 start indices)
+    lo, hi = args.lo, args.hi
+    shard = (rank, world, 64) if world > 1 else None
 
     f = P.parse_system(open(os.path.join(ROOT, "tests", "data", "cyclic10.sys")).read())
     g, st = P.total_degree_start(f, args.prec)
@@ -40,11 +40,13 @@ def main():
     counts = {}
     ends = []
     dev_s = 0.0
+    n_paths = 0
     t0 = time.time()
     for a in range(lo, hi, args.chunk):
         b = min(hi, a + args.chunk)
-        sol = P.track_all(h, st, cfg, lo=a, hi=b, device=device)
+        sol = P.track_all(h, st, cfg, lo=a, hi=b, device=device, shard=shard)
         dev_s += sol.stats["device_ms"] / 1e3
+        n_paths += len(sol)
         for k, v in sol.counts().items():
             counts[k] = counts.get(k, 0) + v
         ends.append(sol.x_complex()[sol.status == P.SUCCESS])
@@ -56,10 +58,10 @@ def main():
     distinct = len(np.unique(key, axis=0)) if len(key) else 0
     if args.out:
         np.save(args.out, x)
-    print(json.dumps({"rank": rank, "world": world, "range": [lo, hi], "paths": hi - lo, "counts": counts,
+    print(json.dumps({"rank": rank, "world": world, "range": [lo, hi], "shard": shard, "paths": n_paths, "counts": counts,
                       "converged": counts.get("converged", 0), "distinct_converged_endpoints": distinct,
-                      "device_s": dev_s, "wall_s": wall, "paths_per_s_device": (hi - lo) / dev_s if dev_s else None,
-                      "paths_per_s_wall": (hi - lo) / wall}), flush=True)
+                      "device_s": dev_s, "wall_s": wall, "paths_per_s_device": n_paths / dev_s if dev_s else None,
+                      "paths_per_s_wall": n_paths / wall}), flush=True)
 
 
 if __name__ == "__main__":

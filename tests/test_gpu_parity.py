@@ -28,10 +28,16 @@ def homotopy(P, text, prec, seed=1, g_text=None):
     return f, g, starts, P.make_homotopy(f, g, P.random_gamma(seed), prec)
 
 
+def bits(a):
+    """bit patterns of a record array (floats compared bit for bit: -0.0 differs from 0.0)"""
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint64) if a.dtype == np.float64 else a
+
+
 def assert_records(sol, g, lo=0):
     assert np.array_equal(sol.path_id, np.arange(lo, lo + len(sol), dtype=np.uint64))
     for k in TRACK_KEYS:
-        got, want = getattr(sol, k), g[k]
+        got, want = bits(getattr(sol, k)), bits(g[k])
         if not np.array_equal(got, want):
             bad = np.flatnonzero(np.any(np.asarray(got).reshape(len(sol), -1) != np.asarray(want).reshape(len(sol), -1), axis=1))
             raise AssertionError(f"{k} differs on {len(bad)} paths, first {bad[:5]}")

@@ -12,16 +12,46 @@ import torch.multiprocessing as mp
 from conftest import ROOT, read
 
 
-def test_shard_range_partitions():
-    from paper_1505_00383_b200.shard import shard_range
+def test_block_cyclic_shards_partition():
+    from paper_1505_00383_b200.shard import contiguous_range, shard_indices, shard_size
 
-    for lo, hi, world in [(0, 120, 2), (5, 6, 4), (0, 0, 3), (100, 1234567, 8), (7, 19, 5)]:
-        parts = [shard_range(lo, hi, r, world) for r in range(world)]
-        assert parts[0][0] == lo and parts[-1][1] == max(lo, hi)
-        for (a, b), (c, d) in zip(parts, parts[1:]):
-            assert b == c
-        sizes = [b - a for a, b in parts]
-        assert max(sizes) - min(sizes) <= 1
+    for lo, hi, world, block in [(0, 120, 2, 64), (5, 6, 4, 1), (0, 0, 3, 8), (100, 12345, 8, 64), (7, 19, 5, 3)]:
+        parts = [shard_indices(lo, hi, r, world, block) for r in range(world)]
+        assert [len(p) for p in parts] == [shard_size(lo, hi, r, world, block) for r in range(world)]
+        allids = np.sort(np.concatenate(parts))
+        assert np.array_equal(allids, np.arange(lo, max(lo, hi), dtype=np.uint64))
+        for p in parts:
+            assert np.all(np.diff(p.astype(np.int64)) > 0)
+        sizes = [len(p) for p in parts]
+        assert max(sizes) - min(sizes) <= block
+        cparts = [contiguous_range(lo, hi, r, world) for r in range(world)]
+        assert cparts[0][0] == lo and cparts[-1][1] == max(lo, hi)
+
+
+def test_shard_size_matches_the_library(pp):
+    """pp_shard_size (C ABI) and the Python mirror agree"""
+    from paper_1505_00383_b200.shard import shard_size
+
+    for lo, hi, world, block in [(0, 120, 2, 64), (5, 6, 4, 1), (100, 12345, 8, 64), (7, 19, 5, 3), (0, 3628800, 8, 64)]:
+        for r in range(world):
+            assert pp.shard_size(lo, hi, (r, world, block)) == shard_size(lo, hi, r, world, block)
+
+
+def test_bench_spawns_one_rank_per_gpu():
+    """`bench.py --gpus 2` outside torchrun launches two ranks itself (torch.distributed.run on
+    127.0.0.1); --launch-check makes each rank report its geometry without GPU work"""
+    import json
+    import re
+    import subprocess
+    import sys
+
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--launch-check"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(m) for m in re.findall(r"\{[^{}]*\}", out.stdout)]
+    assert sorted(d["rank"] for d in lines) == [0, 1]
+    assert all(d["world"] == 2 for d in lines)
+    assert sorted(tuple(d["shard"]) for d in lines) == [(0, 2, 64), (1, 2, 64)]
 
 
 def _free_port():
@@ -42,10 +72,13 @@ def _oracle_track_fn(text, prec):
     plan = O.ref_plan(text, prec, gl)
     cfg = O.ref_defaults(prec)
 
-    def fn(lo, hi):
-        starts = np.stack([O.ref_td_solution(text, prec, i, plan["dim"]) for i in range(lo, hi)])
+    def fn(lo, hi, shard):
+        from paper_1505_00383_b200.shard import shard_indices
+
+        ids = shard_indices(lo, hi, *shard) if shard else np.arange(lo, hi, dtype=np.uint64)
+        starts = np.stack([O.ref_td_solution(text, prec, int(i), plan["dim"]) for i in ids])
         r = O.oracle_track(plan, cfg, starts)
-        r["path_id"] = np.arange(lo, hi, dtype=np.uint64)
+        r["path_id"] = ids
         return r
 
     return fn
@@ -62,7 +95,7 @@ def _worker(rank, world, port, out_dir):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     fn = _oracle_track_fn(read("cyclic5.sys"), "d")
-    merged = distributed_track_all(fn, 3, 120, dist)
+    merged = distributed_track_all(fn, 3, 120, dist, block=16)
     if rank == 0:
         np.savez(os.path.join(out_dir, "merged.npz"), **merged)
     dist.barrier()
