@@ -29,6 +29,9 @@ int pp_test_plan_coeffs(const pp_homotopy* h, double* out, size_t cap);
 int pp_test_plan_tables(const pp_homotopy* h, int which, uint32_t* out, size_t cap, size_t* count);
 /* measured FP64 pipe throughput of a device (DFMA ops/s), the roofline denominator */
 int pp_fp64_peak(int device, double* ops_per_s);
+/* n doubles formatted as the JSON-lines records print them (nlohmann::json 3.11's dump()),
+ * newline-separated; *needed = bytes including the NUL (PP_E_CAPACITY when cap is too small) */
+int pp_test_json_doubles(const double* v, size_t n, char* buf, size_t cap, size_t* needed);
 /* [mon_steps, cmul_steps, jac_terms, jac_scaled, n_base] of a homotopy's plan */
 int pp_homotopy_counts(const pp_homotopy* h, uint64_t* counts);
 

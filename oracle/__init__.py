@@ -36,7 +36,7 @@ def build(reference_root: str = "/root/reference/proj") -> None:
     if os.path.isdir(reference_root):
         # the reference library, and its acceptance suite on the CPU tracker and through the
         # drop-in shim on libpp200.so (needs the CUDA library built first)
-        targets += ["ref", "acceptance"]
+        targets += ["ref", "acceptance", "jsonref"]
     subprocess.run(["make", "-C", HERE, "-j8", f"REF={reference_root}", *targets], check=True,
                    stdout=subprocess.DEVNULL)
 

@@ -159,6 +159,7 @@ _sig("pp_system_parse", _i32, ctypes.c_char_p, _sz, _P(_vp))
 _sig("pp_system_cyclic", _i32, _u32, _P(_vp))
 _sig("pp_system_from_terms", _i32, _u32, _u32, _vp, _vp, _vp, _vp, _P(_vp))
 _sig("pp_device_count", _i32)
+_sig("pp_test_json_doubles", _i32, _vp, _sz, ctypes.c_char_p, _sz, _P(_sz))
 _sig("pp_system_print", _i32, _vp, ctypes.c_char_p, _sz, _P(_sz))
 _sig("pp_system_stats", _i32, _vp, _P(_u32), _P(_u32), _P(_u64), _P(_u64), _P(_i32))
 _sig("pp_system_degrees", _i32, _vp, _vp)

@@ -15,6 +15,7 @@
 #include <string>
 
 #include "device.hpp"
+#include "json_number.hpp"
 #include "host.hpp"
 #include "pp200.h"
 
@@ -495,14 +496,8 @@ int pp_lsq_batch(int prec, uint32_t n, uint32_t batch, const double* a, const do
 }  // extern "C"
 
 namespace {
-// a double as nlohmann::json::dump prints it: shortest round-trip digits, ".0" on integral values
-void put_double(std::string& o, double v) {
-  char b[64];
-  auto r = std::to_chars(b, b + sizeof b, v);
-  std::string t(b, r.ptr);
-  if (t.find_first_of(".eEn") == std::string::npos) t += ".0";
-  o += t;
-}
+// a double as nlohmann::json::dump prints it (json_number.cpp)
+void put_double(std::string& o, double v) { pp::json_double(o, v); }
 std::string limbs_decimal(int prec, const double* p) {
   return prec == PP_D ? pp::to_decimal_d(p[0])
          : prec == PP_DD ? pp::to_decimal_dd(pp::dd_t{p[0], p[1]})
@@ -777,6 +772,19 @@ int pp_test_plan_tables(const pp_homotopy* h, int which, uint32_t* out, size_t c
   *count = v->size();
   if (out == nullptr || cap < v->size()) return PP_E_CAPACITY;
   std::copy(v->begin(), v->end(), out);
+  return PP_OK;
+}
+
+// doubles formatted as the JSON records print them (json_number.cpp), newline-separated
+int pp_test_json_doubles(const double* v, size_t n, char* buf, size_t cap, size_t* needed) {
+  std::string o;
+  for (size_t i = 0; i < n; ++i) {
+    pp::json_double(o, v[i]);
+    o += '\n';
+  }
+  if (needed) *needed = o.size() + 1;
+  if (buf == nullptr || cap < o.size() + 1) return PP_E_CAPACITY;
+  std::memcpy(buf, o.c_str(), o.size() + 1);
   return PP_OK;
 }
 

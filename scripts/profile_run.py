@@ -41,7 +41,10 @@ def sample():
 th = threading.Thread(target=sample, daemon=True)
 th.start()
 t0 = time.time()
-sol = P.track_all(h, st, P.TrackConfig.defaults(prec), lo=offset, hi=offset + paths)
+cfg = P.TrackConfig.defaults(prec)
+if os.environ.get("MAX_NEWTON"):
+    cfg.max_newton = int(os.environ["MAX_NEWTON"])
+sol = P.track_all(h, st, cfg, lo=offset, hi=offset + paths)
 wall = time.time() - t0
 stop.set()
 th.join()
