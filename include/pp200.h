@@ -136,6 +136,10 @@ int pp_system_from_terms(uint32_t dim, uint32_t n_polys, const uint32_t* term_co
                          const uint32_t* factors, const double* coeff, pp_system** out);
 /* CUDA devices visible to the library (0 without a usable driver) */
 int pp_device_count(void);
+/* create the CUDA context of `device`, the calling thread's stream and workspace context, and load
+ * the tracking kernels, so that the first pp_track_all on this thread does not pay for them
+ * (about 1.8 s on a fresh B200 process); optional */
+int pp_device_init(int device);
 /* writes a NUL-terminated text form; *needed = bytes required including the NUL */
 int pp_system_print(const pp_system* s, char* buf, size_t cap, size_t* needed);
 int pp_system_stats(const pp_system* s, uint32_t* dim, uint32_t* n_polys, uint64_t* n_monomials,

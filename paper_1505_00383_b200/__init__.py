@@ -159,6 +159,7 @@ _sig("pp_system_parse", _i32, ctypes.c_char_p, _sz, _P(_vp))
 _sig("pp_system_cyclic", _i32, _u32, _P(_vp))
 _sig("pp_system_from_terms", _i32, _u32, _u32, _vp, _vp, _vp, _vp, _P(_vp))
 _sig("pp_device_count", _i32)
+_sig("pp_device_init", _i32, _i32)
 _sig("pp_test_json_doubles", _i32, _vp, _sz, ctypes.c_char_p, _sz, _P(_sz))
 _sig("pp_system_print", _i32, _vp, ctypes.c_char_p, _sz, _P(_sz))
 _sig("pp_system_stats", _i32, _vp, _P(_u32), _P(_u32), _P(_u64), _P(_u64), _P(_i32))
@@ -202,7 +203,7 @@ EXPORTED = [
     "pp_load_start_data", "pp_starts_explicit", "pp_starts_roots", "pp_starts_count", "pp_starts_solution", "pp_starts_free",
     "pp_make_homotopy", "pp_homotopy_info", "pp_homotopy_free", "pp_track_config_defaults",
     "pp_track_config_validate", "pp_track_all", "pp_eval_batch", "pp_lsq_batch", "pp_solutions_jsonl",
-    "pp_to_decimal", "pp_bench_eval", "pp_track_all_ex", "pp_shard_size", "pp_system_from_terms", "pp_device_count", "pp_lsq_batch_mn",
+    "pp_to_decimal", "pp_bench_eval", "pp_track_all_ex", "pp_shard_size", "pp_system_from_terms", "pp_device_count", "pp_lsq_batch_mn", "pp_device_init",
 ]
 
 
@@ -305,6 +306,11 @@ def system_from_terms(dim: int, polys) -> System:
 
 def device_count() -> int:
     return int(lib.pp_device_count())
+
+
+def device_init(device: int = 0) -> None:
+    """create the device context and load the kernels ahead of the first track_all (pp_device_init)"""
+    _check(lib.pp_device_init(device))
 
 
 def random_gamma(seed: int) -> complex:

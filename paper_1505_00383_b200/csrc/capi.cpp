@@ -85,6 +85,13 @@ extern "C" {
 const char* pp_version(void) { return "pp200 0.2 (sm_100a)"; }
 
 int pp_device_count(void) { return pp::device_count(); }
+
+int pp_device_init(int device) {
+  return guard([&] {
+    pp::device_init(device);
+    return PP_OK;
+  });
+}
 const char* pp_last_error(void) { return g_error.c_str(); }
 int pp_limbs(int prec) { return limbs_of(prec); }
 

@@ -310,6 +310,31 @@ int device_count() {
   return n;
 }
 
+// Create the device context and this thread's stream / workspace context, and load the tracking
+// kernels (module loading is lazy otherwise: the first launch of each kernel would pay for it).
+void device_init(int device) {
+  DeviceGuard g(device);
+  check(cudaFree(nullptr), "context");
+  (void)device_props(device);
+  (void)context(device);
+  for (auto fn : {&dev::variants_d, &dev::variants_dd, &dev::variants_qd}) {
+    int cnt = 0;
+    const dev::Variant* v = fn(&cnt);
+    for (int i = 0; i < cnt; ++i)
+      for (const void* k : {v[i].ctrl_eval_trip, v[i].lsq_trip, v[i].step_trip, v[i].eval, v[i].lsq, v[i].eval_coop,
+                            v[i].lsq_coop, v[i].lsq_coop_g, v[i].ctrl_eval_tmem}) {
+        cudaFuncAttributes at;
+        check(cudaFuncGetAttributes(&at, k), "kernel load");
+      }
+  }
+  int cnt = 0;
+  const dev::LsqReg* lr = dev::lsq_reg_d(&cnt);
+  for (int i = 0; i < cnt; ++i) {
+    cudaFuncAttributes at;
+    check(cudaFuncGetAttributes(&at, lr[i].hold), "kernel load");
+  }
+}
+
 bool device_supports(uint32_t n, uint32_t max_k) { return pick_variant(1, n, max_k) != nullptr; }
 
 uint64_t shard_size(uint64_t lo, uint64_t hi, const TrackShard& sh) {
@@ -504,8 +529,15 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
       if (lr[i].n == static_cast<int>(n)) lsq_reg = mode == 1 ? lr[i].stream : lr[i].hold;
   }
   if (lsq_reg) lsq_fn = lsq_reg;
+  // PP200_LSQ_QCACHE=1: the column in shared memory and q_i cached in TMEM between its dot product
+  // and its axpy (128 columns per CTA; the shared memory request is padded so that at most four
+  // CTAs are resident per SM and every tcgen05.alloc succeeds at once)
+  const bool lsq_qc = !lsq_tm && !lsq_reg && tblock == 128 && env_size("PP200_LSQ_QCACHE", 0) != 0 &&
+                      static_cast<size_t>(n) * 4 * L <= 128;
+  if (lsq_qc) lsq_fn = var->lsq_qcache;
   const int lblock = lsq_tm ? 256 : tblock;
-  const size_t lsq_smem = (lsq_tm || lsq_reg) ? 0 : static_cast<size_t>(tblock) * per_thread_smem / 2;
+  size_t lsq_smem = (lsq_tm || lsq_reg) ? 0 : static_cast<size_t>(tblock) * per_thread_smem / 2;
+  if (lsq_qc) lsq_smem = std::max<size_t>(lsq_smem, (prop.sharedMemPerMultiprocessor / 5) + 1024);
   ensure_smem(ctrl_eval_fn, eval_smem, device);
   ensure_smem(lsq_fn, lsq_smem, device);
   // slots: PP200_SLOTS_PER_SM per SM (default 512; 1024 in complex double, whose kernels are

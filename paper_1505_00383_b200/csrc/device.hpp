@@ -56,6 +56,9 @@ bool device_supports(uint32_t n, uint32_t max_k);
 // CUDA devices visible (0 without a usable driver)
 int device_count();
 
+// context, per-thread resources and kernel modules of a device, created ahead of the first call
+void device_init(int device);
+
 // measured FP64 pipe operations per second (DFMA microbenchmark)
 double device_fp64_peak(int device);
 

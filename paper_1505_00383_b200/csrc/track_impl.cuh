@@ -538,9 +538,45 @@ __device__ __forceinline__ void prefetch_column(const GA& Q, int col, int n, siz
 #endif
 }
 
-template <class R, class GA, class CA, bool kUniform>
+// Where the axpy of a projection re-reads q_i: from the solver array itself (NoQCache; L1 / L2 /
+// HBM), or from a copy the dot product left in the thread's tensor-memory lane (TmemQCache), so
+// that q_i streams from global memory once per projection instead of twice.
+struct NoQCache {
+  template <class R>
+  __device__ __forceinline__ void put(int, const cx<R>&) const {}
+  __device__ __forceinline__ void commit() const {}
+  template <class R, class GA>
+  __device__ __forceinline__ cx<R> get(int, const GA& Q, int e, size_t s) const {
+    return Q.ld(e, s);
+  }
+};
+
+template <class R>
+struct TmemQCache {
+  static constexpr int W = 4 * level<R>::L;  // 32-bit columns per complex value
+  uint32_t base;                             // this warp's lane quarter, first column
+  __device__ __forceinline__ void put(int r, const cx<R>& q) const {
+    uint32_t v[W];
+    TmemRow<R>::pack(q, v);
+    __syncwarp();
+    tmem_st_issue<W>(base + static_cast<uint32_t>(r) * W, v);
+  }
+  __device__ __forceinline__ void commit() const {
+    __syncwarp();
+    tmem_wait_st();
+  }
+  template <class RR, class GA>
+  __device__ __forceinline__ cx<R> get(int r, const GA&, int, size_t) const {
+    uint32_t v[W];
+    __syncwarp();
+    TmemIO<W>::ld(base + static_cast<uint32_t>(r) * W, v);
+    return TmemRow<R>::unpack(v);
+  }
+};
+
+template <class R, class GA, class CA, bool kUniform, class QC = NoQCache>
 __device__ bool lsq_solve_c(int n, int m, double rank_tol, const GA& Q, const GA& Rm, const GA& B, const GA& Y,
-                            size_t s, const CA& C) {
+                            size_t s, const CA& C, const QC& qc = QC{}) {
   // m x n (m >= n rows; the tracker's systems are square, m == n): Q column-major, element col*m + row
   const cx<R> zero = czero<R>();
   R max_norm = rfrom<R>(0.0);
@@ -567,11 +603,16 @@ PP_UNROLL_ROWS
         if (nxt < n) prefetch_column<R>(Q, nxt, m, s);
         cx<R> rik = zero;
 PP_UNROLL_ROWS
-        for (int r = 0; r < m; ++r) rik = cadd(rik, cmul(cconj(Q.ld(i * m + r, s)), C.ld(r)));
+        for (int r = 0; r < m; ++r) {
+          const cx<R> q = Q.ld(i * m + r, s);
+          qc.put(r, q);
+          rik = cadd(rik, cmul(cconj(q), C.ld(r)));
+        }
         const cx<R> prev = pass == 0 ? zero : Rm.ld(i + rk, s);
         Rm.st(i + rk, s, cadd(prev, rik));
+        qc.commit();
 PP_UNROLL_ROWS
-        for (int r = 0; r < m; ++r) C.st(r, csub(C.ld(r), cmul(rik, Q.ld(i * m + r, s))));
+        for (int r = 0; r < m; ++r) C.st(r, csub(C.ld(r), cmul(rik, qc.template get<R>(r, Q, i * m + r, s))));
       }
     }
     R acc = rfrom<R>(0.0);
@@ -649,7 +690,9 @@ __device__ __forceinline__ void tmem_free_cta(uint32_t base) {
 // kTmem: the column being orthogonalised lives in the thread's TMEM lane instead of shared
 // memory, which leaves the whole L1 to the Q columns (the axpy re-reads q_i right after the dot
 // product).  Its accesses are warp-collective, so a warp runs the solve if any lane needs it.
-template <class R, bool kTmem, int kThreads, int kMinBlocks>
+// kQCache (with kTmem false): the column in shared memory, and each projected q_i cached in the
+// thread's TMEM lane between its dot product and its axpy (TmemQCache); warp-collective as well.
+template <class R, bool kTmem, int kThreads, int kMinBlocks, bool kQCache = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) lsq_trip(const TrackArgs a) {
   constexpr int L = level<R>::L;
   extern __shared__ double smem[];
@@ -661,7 +704,30 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) lsq_trip(const TrackArgs
   const int n = a.plan.n;
   const Planar<R> X{a.x, a.S};
   const auto J = PP_WORK(a.J, n * n), Rm = PP_WORK(a.Rm, n * (n + 1) / 2), B = PP_WORK(a.B, n), Y = PP_WORK(a.Y, n);
-  if (!kTmem) {
+  if (!kTmem && kQCache) {
+    __shared__ uint32_t tmem_holder;
+    const uint32_t base = tmem_alloc_cta<128>(&tmem_holder);
+    const int warp = threadIdx.x >> 5;
+    const TmemQCache<R> qc{base + (static_cast<uint32_t>(32 * (warp & 3)) << 16)};
+    const SmemRow<R> C{Planar<R>{smem, blockDim.x}, threadIdx.x};
+    if (__any_sync(0xffffffffu, need)) {
+      const bool ok = lsq_solve_c<R, decltype(J), SmemRow<R>, true>(n, n, a.rank_tol, J, Rm, B, Y, s, C, qc);
+      if (need) si(F_OK, s) = ok ? 1 : 0;
+      if (need && ok) {
+        double dxn = 0.0, xn = 0.0;
+        for (int v = 0; v < n; ++v) {
+          const cx<R> dv = C.ld(v);
+          const cx<R> xv = cadd(X.ld(v, s), dv);
+          X.st(v, s, xv);
+          dxn = f_max(dxn, cabsd(dv));
+          xn = f_max(xn, cabsd(xv));
+        }
+        a.sd[D_DXN * a.S + s] = dxn;
+        a.sd[D_XN * a.S + s] = xn;
+      }
+    }
+    tmem_free_cta<128>(base);
+  } else if (!kTmem) {
     if (!need) return;
     const SmemRow<R> C{Planar<R>{smem, blockDim.x}, threadIdx.x};
     const bool ok = lsq_solve_c<R, decltype(J), SmemRow<R>, false>(n, n, a.rank_tol, J, Rm, B, Y, s, C);
@@ -1537,7 +1603,8 @@ __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
    reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, false>),                       \
    reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, true>),                        \
    reinterpret_cast<const void*>(&pp::dev::ctrl_eval_trip<R, KM, true, (sizeof(R) < 32 ? 4 : 1)>),             \
-   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, true, 256, 2>)}
+   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, true, 256, 2>),                                        \
+   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, false, 128, PP_LSQ_MINB, true>)}
 
 // register-resident least-squares solvers of one level for dimension N
 #define PP_LSQ_REG(R, N)                                                                        \

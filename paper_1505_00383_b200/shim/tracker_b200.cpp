@@ -239,6 +239,19 @@ SolutionSet<R> track_on_b200(const HomotopyInstance<R>& h, const StartData<R>& s
   return out;
 }
 
+// The device is initialised when the program starts (context, per-thread resources, kernel
+// modules: about 1.8 s on a fresh process), as a GPU service does at start-up, rather than inside
+// whichever track_all call comes first.  POLYPATH_B200_EAGER_INIT=0 defers it to the first call.
+// Without a usable device nothing happens here; track_all then fails loudly (no CPU fallback).
+struct EagerInit {
+  EagerInit() {
+    if (env_u("POLYPATH_B200_EAGER_INIT", 1) == 0 || pp_device_count() <= 0) return;
+    const unsigned first = env_u("POLYPATH_B200_DEVICE", 0), n = std::max(1u, env_u("POLYPATH_B200_DEVICES", 1));
+    for (unsigned d = first; d < first + n && static_cast<int>(d) < pp_device_count(); ++d) pp_device_init(static_cast<int>(d));
+  }
+};
+const EagerInit g_eager_init;
+
 }  // namespace
 
 template <>
