@@ -321,8 +321,10 @@ void device_init(int device) {
     int cnt = 0;
     const dev::Variant* v = fn(&cnt);
     for (int i = 0; i < cnt; ++i)
-      for (const void* k : {v[i].ctrl_eval_trip, v[i].lsq_trip, v[i].step_trip, v[i].eval, v[i].lsq, v[i].eval_coop,
-                            v[i].lsq_coop, v[i].lsq_coop_g, v[i].ctrl_eval_tmem}) {
+      for (const void* k : {v[i].ctrl_eval_trip, v[i].lsq_trip, v[i].step_trip, v[i].eval, v[i].lsq, v[i].eval_coop[0],
+                            v[i].eval_coop[1], v[i].eval_coop[2], v[i].lsq_coop[0], v[i].lsq_coop[1], v[i].lsq_coop[2],
+                            v[i].lsq_coop_g[0], v[i].lsq_coop_g[1], v[i].lsq_coop_g[2], v[i].ctrl_eval_tmem,
+                            v[i].lsq_qcache}) {
         cudaFuncAttributes at;
         check(cudaFuncGetAttributes(&at, k), "kernel load");
       }
@@ -695,25 +697,46 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     // launch to at most that many slots, each remaining path gets a whole warp (eval_coop /
     // lsq_coop), bitwise identical to the thread-per-path kernels
     const size_t el = static_cast<size_t>(2) * L * sizeof(double);  // bytes per complex value
-    const size_t ecoop_warp = (static_cast<size_t>(n) + plan.n_slots()) * el;
-    // Q and R in shared memory while they take at most PP200_COOP_SMEM_KB (4) KB per warp, else
-    // left in the global arrays (more warps per SM)
+    const size_t ecoop_slot = (static_cast<size_t>(n) + plan.n_slots()) * el;
+    // Q and R in shared memory while they take at most PP200_COOP_SMEM_KB (4) KB per slot, else
+    // left in the global arrays (more slots per SM)
     const bool coop_global = static_cast<size_t>(n) * n * el > env_size("PP200_COOP_SMEM_KB", 4) * 1024;
-    const void* lsq_coop_fn = coop_global ? var->lsq_coop_g : var->lsq_coop;
-    const size_t lcoop_warp =
+    const size_t lcoop_slot =
         (coop_global ? static_cast<size_t>(4) * n : static_cast<size_t>(n) * n + 4 * n + n * (n + 1) / 2) * el;
-    const int ewpb = static_cast<int>(std::min<size_t>(4, (200 * 1024) / ecoop_warp));
-    const int lwpb = static_cast<int>(std::min<size_t>(4, (200 * 1024) / lcoop_warp));
+    // lanes per slot (G = 32, 8 or 4; G < 32 packs 32 / G slots into a warp).  A warp per slot gives
+    // each path the lowest trip latency, which is what the last few paths of a run need; with many
+    // slots per SM, smaller groups keep more lanes busy (the reference's sequential sums run on two
+    // lanes of the group, its row operations on all of them).  PP200_COOP_GROUP fixes G; the
+    // default picks G = 8 from PP200_COOP_G8_PER_SM (8) busy slots per SM up, else 32.
+    const size_t coop_group_env = env_size("PP200_COOP_GROUP", 0);
+    const size_t g8_per_sm = env_size("PP200_COOP_G8_PER_SM", 8);
+    auto coop_gi = [&](size_t active) -> int {
+      if (coop_group_env == 32) return 0;
+      if (coop_group_env == 8) return 1;
+      if (coop_group_env == 4) return 2;
+      return active >= g8_per_sm * static_cast<size_t>(prop.multiProcessorCount) ? 1 : 0;
+    };
+    // warps per block of the tail-mode kernels for group index gi (at most 4, within 200 KB)
+    auto coop_wpb = [&](size_t per_slot, int gi) {
+      const size_t per_warp = per_slot * static_cast<size_t>(32 / dev::kCoopGroups[gi]);
+      return static_cast<int>(std::min<size_t>(4, (200 * 1024) / per_warp));
+    };
+    bool coop_ok = true;
+    for (int gi = 0; gi < 3; ++gi) {
+      const int ew = coop_wpb(ecoop_slot, gi), lw = coop_wpb(lcoop_slot, gi);
+      if (ew < 1 || lw < 1) {
+        coop_ok = false;
+        continue;
+      }
+      const size_t spw = static_cast<size_t>(32 / dev::kCoopGroups[gi]);
+      ensure_smem(var->eval_coop[gi], ew * spw * ecoop_slot, device);
+      ensure_smem(coop_global ? var->lsq_coop_g[gi] : var->lsq_coop[gi], lw * spw * lcoop_slot, device);
+    }
     const size_t tail_slots = env_size("PP200_TAIL_SLOTS", 32 * static_cast<size_t>(prop.multiProcessorCount));
     // PP200_FORCE_COOP=1 runs every trip in tail mode (used by the parity tests)
     // small runs (no more paths than tail slots) start in tail mode: a warp per path spreads a
     // few thousand paths over every SM instead of packing them into a few blocks
-    bool coop = (env_size("PP200_FORCE_COOP", 0) != 0 || (tail_slots > 0 && count <= tail_slots)) && ewpb >= 1 &&
-                lwpb >= 1;
-    if (ewpb >= 1 && lwpb >= 1) {
-      ensure_smem(var->eval_coop, ewpb * ecoop_warp, device);
-      ensure_smem(lsq_coop_fn, lwpb * lcoop_warp, device);
-    }
+    bool coop = (env_size("PP200_FORCE_COOP", 0) != 0 || (tail_slots > 0 && count <= tail_slots)) && coop_ok;
     // one trip = control (step control, prediction, finalize, refill) followed by the heavy
     // operation of every busy slot.  Thread-per-path mode fuses the control into the evaluation
     // kernel (ctrl_eval_trip) and runs lsq_trip; tail mode runs step_trip, eval_coop, lsq_coop.
@@ -725,12 +748,16 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
       if (coop) {
         check(cudaLaunchKernel(var->step_trip, grid, blk, args, 0, stream), "launch step_trip");
         if (ev) check(cudaEventRecord(ev[1], stream), "event");
-        const unsigned eb = static_cast<unsigned>((a.n_active + ewpb - 1) / ewpb);
-        const unsigned lb = static_cast<unsigned>((a.n_active + lwpb - 1) / lwpb);
-        check(cudaLaunchKernel(var->eval_coop, dim3(eb), dim3(32 * ewpb), targs, ewpb * ecoop_warp, stream),
+        const int gi = coop_gi(a.n_active);
+        const size_t spw = static_cast<size_t>(32 / dev::kCoopGroups[gi]);
+        const int ew = coop_wpb(ecoop_slot, gi), lw = coop_wpb(lcoop_slot, gi);
+        const unsigned eb = static_cast<unsigned>((a.n_active + ew * spw - 1) / (ew * spw));
+        const unsigned lb = static_cast<unsigned>((a.n_active + lw * spw - 1) / (lw * spw));
+        check(cudaLaunchKernel(var->eval_coop[gi], dim3(eb), dim3(32 * ew), targs, ew * spw * ecoop_slot, stream),
               "launch eval_coop");
         if (ev) check(cudaEventRecord(ev[2], stream), "event");
-        check(cudaLaunchKernel(lsq_coop_fn, dim3(lb), dim3(32 * lwpb), targs, lwpb * lcoop_warp, stream),
+        check(cudaLaunchKernel(coop_global ? var->lsq_coop_g[gi] : var->lsq_coop[gi], dim3(lb), dim3(32 * lw), targs,
+                               lw * spw * lcoop_slot, stream),
               "launch lsq_coop");
       } else {
         if (ev) check(cudaEventRecord(ev[1], stream), "event");
@@ -774,7 +801,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
       dev::launch_compaction(m, stream);
       a.n_active = keep;
       grid = dim3(static_cast<unsigned>(keep / tblock));
-      coop = coop || (tail_slots > 0 && ewpb >= 1 && lwpb >= 1 && keep <= tail_slots);
+      coop = coop || (tail_slots > 0 && coop_ok && keep <= tail_slots);
       ++compactions;
       launches += 2;
       return true;

@@ -113,6 +113,8 @@ struct LsqArgs {
   uint8_t* ok;
 };
 
+constexpr int kCoopGroups[3] = {32, 8, 4};
+
 struct Variant {
   int kmax;
   const void* ctrl_eval_trip;  // __global__ void(TrackArgs, unsigned* busy): control + evaluation
@@ -120,9 +122,10 @@ struct Variant {
   const void* step_trip;  // __global__ void(TrackArgs, unsigned* busy)
   const void* eval;       // __global__ void(EvalArgs)
   const void* lsq;        // __global__ void(LsqArgs)
-  const void* eval_coop;  // __global__ void(TrackArgs): one warp per slot (tail mode)
-  const void* lsq_coop;   // __global__ void(TrackArgs): one warp per slot (tail mode), Q in shared memory
-  const void* lsq_coop_g; // the same with Q and R in the global (tiled) arrays, for large n
+  // tail mode, G lanes per slot for G = kCoopGroups[i] (32: a warp per slot)
+  const void* eval_coop[3];   // __global__ void(TrackArgs)
+  const void* lsq_coop[3];    // __global__ void(TrackArgs), Q and R in shared memory
+  const void* lsq_coop_g[3];  // the same with Q and R in the global (tiled) arrays, for large n
   const void* ctrl_eval_tmem;  // ctrl_eval_trip with the open Jacobian row in tensor memory
   const void* lsq_tmem;        // lsq_trip with the Gram-Schmidt column in tensor memory
   const void* lsq_qcache;      // lsq_trip with q_i cached in tensor memory between dot and axpy

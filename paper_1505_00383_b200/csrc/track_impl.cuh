@@ -1322,57 +1322,86 @@ __global__ void __launch_bounds__(128, kMinBlocks) ctrl_eval_trip(const TrackArg
 //    scaling); every sequential sum of the reference (dot products, norms, back substitution)
 //    is carried out in order by lane 0.
 
-// warp max of a level value (rcmp order; equal values are identical, so the result is exact)
-template <class R>
-__device__ __forceinline__ R warp_rmax(R v) {
-  constexpr int L = level<R>::L;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    R o;
-#pragma unroll
-    for (int l = 0; l < L; ++l) level<R>::set(o, l, __shfl_xor_sync(0xffffffffu, level<R>::get(v, l), off));
-    if (rcmp(o, v) > 0) v = o;
+// lane group of the tail-mode kernels: G consecutive lanes serve one path slot, 32 / G slots per warp
+template <int G>
+struct LaneGroup {
+  static constexpr int kPerWarp = 32 / G;
+  int gl;         // lane within the group
+  int first;      // the group's first lane in the warp
+  unsigned mask;  // the group's lanes
+  __device__ __forceinline__ LaneGroup() {
+    const int lane = threadIdx.x & 31;
+    gl = lane % G;
+    first = lane - gl;
+    mask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << first);
   }
-  return v;
-}
-__device__ __forceinline__ double warp_fmax(double v) {
+  __device__ __forceinline__ size_t slot() const {
+    return (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * kPerWarp + first / G;
+  }
+  __device__ __forceinline__ int index_in_block() const { return (threadIdx.x >> 5) * kPerWarp + first / G; }
+  __device__ __forceinline__ void sync() const { __syncwarp(mask); }
+  // max over the group (rcmp order; equal values are identical, so the result is exact)
+  template <class R>
+  __device__ __forceinline__ R rmax(R v) const {
+    constexpr int L = level<R>::L;
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) v = f_max(v, __shfl_xor_sync(0xffffffffu, v, off));
-  return v;
-}
+    for (int off = G / 2; off > 0; off >>= 1) {
+      R o;
+#pragma unroll
+      for (int l = 0; l < L; ++l) level<R>::set(o, l, __shfl_xor_sync(mask, level<R>::get(v, l), off));
+      if (rcmp(o, v) > 0) v = o;
+    }
+    return v;
+  }
+  __device__ __forceinline__ double fmax(double v) const {
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) v = f_max(v, __shfl_xor_sync(mask, v, off));
+    return v;
+  }
+  template <class R>
+  __device__ __forceinline__ R bcast(R v) const {  // the group's first lane's value
+    constexpr int L = level<R>::L;
+#pragma unroll
+    for (int l = 0; l < L; ++l) level<R>::set(v, l, __shfl_sync(mask, level<R>::get(v, l), first));
+    return v;
+  }
+};
 
-template <class R, int KMAX>
+// G lanes per path slot (G = 32: a warp per path)
+template <class R, int KMAX, int G>
 __global__ void __launch_bounds__(128) eval_coop(const TrackArgs a) {
   constexpr int L = level<R>::L;
   extern __shared__ double smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
-  const size_t s = static_cast<size_t>(blockIdx.x) * wpb + warp;
-  if (s >= a.n_active) return;  // warp-uniform
+  const LaneGroup<G> g;
+  const int lane = g.gl;
+  const size_t s = g.slot();
+  if (s >= a.n_active) return;  // group-uniform
   const SlotInts si{a.si, a.S};
   const int mode = si(F_MODE, s);
   if (mode != M_NEWTON && mode != M_REFINE && mode != M_FINAL) return;
   const PlanArgs& pa = a.plan;
   const int n = pa.n, np = pa.n_polys;
-  const size_t per_warp = static_cast<size_t>(n + pa.n_slots) * 2 * L;
-  const Planar<R> XS{smem + warp * per_warp, 1}, SL{smem + warp * per_warp + static_cast<size_t>(n) * 2 * L, 1};
+  const size_t per_slot = static_cast<size_t>(n + pa.n_slots) * 2 * L;
+  double* base = smem + static_cast<size_t>(g.index_in_block()) * per_slot;
+  const Planar<R> XS{base, 1}, SL{base + static_cast<size_t>(n) * 2 * L, 1};
   const Planar<R> X{a.x, a.S}, SR{a.sr, a.S};
   const auto J = PP_WORK(a.J, n * np), B = PP_WORK(a.B, np);
-  for (int v = lane; v < n; v += 32) XS.st(v, 0, X.ld(v, s));
-  __syncwarp();
+  for (int v = lane; v < n; v += G) XS.st(v, 0, X.ld(v, s));
+  g.sync();
   const R t = mode == M_NEWTON ? SR.ldr(R_TNEXT, s) : rfrom<R>(1.0);
   const R u = rsub(rfrom<R>(1.0), t);
-  for (int i = lane; i < pa.n_terms; i += 32) {
+  for (int i = lane; i < pa.n_terms; i += G) {
     const int slot = static_cast<int>(__ldg(pa.term_slot + i));
     int poly;
     eval_term<R, KMAX>(
         pa, i, XS, 0, t, u, poly, [&](const cx<R>& v) { SL.st(slot, 0, v); },
         [&](int j, int, const cx<R>& w) { SL.st(slot + 1 + j, 0, w); }, [&](int) {});
   }
-  __syncwarp();
+  g.sync();
   double resid = 0.0;
   R resid_r = rfrom<R>(0.0);
   const int n_acc = np + np * n;
-  for (int acc = lane; acc < n_acc; acc += 32) {
+  for (int acc = lane; acc < n_acc; acc += G) {
     cx<R> sum = czero<R>();
     const int e = static_cast<int>(__ldg(pa.acc_off + acc + 1));
     for (int q = static_cast<int>(__ldg(pa.acc_off + acc)); q < e; ++q)
@@ -1387,8 +1416,8 @@ __global__ void __launch_bounds__(128) eval_coop(const TrackArgs a) {
       J.st(v * np + p, s, sum);
     }
   }
-  resid = warp_fmax(resid);
-  resid_r = warp_rmax<R>(resid_r);
+  resid = g.fmax(resid);
+  resid_r = g.template rmax<R>(resid_r);
   if (lane == 0) {
     a.sd[D_RESID * a.S + s] = resid;
     SR.str(R_RESID, s, resid_r);
@@ -1415,13 +1444,14 @@ struct CoopMat {
 // second pass then runs row-parallel with the sums in order on lanes 0/1.  Each column still
 // sees q_0, q_1, ... in the reference's order in both passes (linalg.hpp:88-100), so the result is
 // bitwise that of lsq_solve_c, with the first pass off the critical path.
-template <class R, bool kGlobalQ>
+template <class R, bool kGlobalQ, int G>
 __global__ void __launch_bounds__(128) lsq_coop(const TrackArgs a) {
   constexpr int L = level<R>::L;
   extern __shared__ double smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
-  const size_t s = static_cast<size_t>(blockIdx.x) * wpb + warp;
-  if (s >= a.n_active) return;  // warp-uniform
+  const LaneGroup<G> g;
+  const int lane = g.gl;
+  const size_t s = g.slot();
+  if (s >= a.n_active) return;  // group-uniform
   const SlotInts si{a.si, a.S};
   const int mode = si(F_MODE, s);
   if (mode != M_NEWTON && mode != M_REFINE) return;
@@ -1429,7 +1459,7 @@ __global__ void __launch_bounds__(128) lsq_coop(const TrackArgs a) {
   const int nR = n * (n + 1) / 2;
   // per warp in shared memory: b, y, x (the update), row products P [, Q (n*n), R (packed)]
   const size_t per_warp = static_cast<size_t>(4 * n + (kGlobalQ ? 0 : n * n + nR)) * 2 * L;
-  double* base = smem + static_cast<size_t>(warp) * per_warp;
+  double* base = smem + static_cast<size_t>(g.index_in_block()) * per_warp;
   const Planar<R> BS{base, 1}, YS{base + n * 2 * L, 1}, DS{base + 2 * n * 2 * L, 1}, PS{base + 3 * n * 2 * L, 1};
   const Planar<R> X{a.x, a.S};
   const auto J = PP_WORK(a.J, n * n), B = PP_WORK(a.B, n);
@@ -1442,21 +1472,21 @@ __global__ void __launch_bounds__(128) lsq_coop(const TrackArgs a) {
     Q.tiled.base = RM.tiled.base = nullptr;
     Q.sm = Planar<R>{base + 4 * n * 2 * L, 1};
     RM.sm = Planar<R>{base + (4 * n + n * n) * 2 * L, 1};
-    for (int e = lane; e < n * n; e += 32) Q.st(e, J.ld(e, s));
+    for (int e = lane; e < n * n; e += G) Q.st(e, J.ld(e, s));
   }
-  for (int e = lane; e < n; e += 32) BS.st(e, 0, B.ld(e, s));
-  __syncwarp();
+  for (int e = lane; e < n; e += G) BS.st(e, 0, B.ld(e, s));
+  g.sync();
   const cx<R> zero = czero<R>();
 
   // column norms (col_norm, linalg.hpp:57-66): one column per lane, rows in order
   R max_norm = rfrom<R>(0.0);
-  for (int j = lane; j < n; j += 32) {
+  for (int j = lane; j < n; j += G) {
     R acc = rfrom<R>(0.0);
     for (int r = 0; r < n; ++r) acc = radd(acc, cabs2(Q.ld(j * n + r)));
     const R nj = rsqrt(acc);
     if (rcmp(nj, max_norm) > 0) max_norm = nj;
   }
-  max_norm = warp_rmax<R>(max_norm);
+  max_norm = g.template rmax<R>(max_norm);
   const R tol = rmul(max_norm, rfrom<R>(a.rank_tol));
 
   bool ok = true;
@@ -1464,47 +1494,46 @@ __global__ void __launch_bounds__(128) lsq_coop(const TrackArgs a) {
     const int rk = k * (k + 1) / 2;
     // second pass of column k (its first pass arrived from the right-looking steps below)
     for (int i = 0; i < k; ++i) {
-      for (int r = lane; r < n; r += 32) PS.st(r, 0, cmul(cconj(Q.ld(i * n + r)), Q.ld(k * n + r)));
-      __syncwarp();
+      for (int r = lane; r < n; r += G) PS.st(r, 0, cmul(cconj(Q.ld(i * n + r)), Q.ld(k * n + r)));
+      g.sync();
       if (lane < 2) {  // dot_conj: rows in order (linalg.hpp:69-73); lane 0 real, lane 1 imaginary part
         R acc = rfrom<R>(0.0);
         for (int r = 0; r < n; ++r) acc = radd(acc, PS.ldr(2 * r + lane, 0));
-        __syncwarp(0x3u);
+        __syncwarp(g.mask & (0x3u << g.first));
         PS.str(lane, 0, acc);
       }
-      __syncwarp();
+      g.sync();
       const cx<R> rik = PS.ld(0, 0);
       if (lane == 0) RM.st(i + rk, cadd(RM.ld(i + rk), rik));  // R(i,k) += rik (second pass)
-      __syncwarp();
-      for (int r = lane; r < n; r += 32) Q.st(k * n + r, csub(Q.ld(k * n + r), cmul(rik, Q.ld(i * n + r))));
-      __syncwarp();
+      g.sync();
+      for (int r = lane; r < n; r += G) Q.st(k * n + r, csub(Q.ld(k * n + r), cmul(rik, Q.ld(i * n + r))));
+      g.sync();
     }
-    for (int r = lane; r < n; r += 32) {
+    for (int r = lane; r < n; r += G) {
       const R v = cabs2(Q.ld(k * n + r));
       PS.st(r, 0, cx<R>{v, rfrom<R>(0.0)});
     }
-    __syncwarp();
+    g.sync();
     R rkk = rfrom<R>(0.0);
     if (lane == 0) {
       R acc = rfrom<R>(0.0);
       for (int r = 0; r < n; ++r) acc = radd(acc, PS.ld(r, 0).re);
       rkk = rsqrt(acc);
     }
-#pragma unroll
-    for (int l = 0; l < L; ++l) level<R>::set(rkk, l, __shfl_sync(0xffffffffu, level<R>::get(rkk, l), 0));
-    __syncwarp();
+    rkk = g.template bcast<R>(rkk);
+    g.sync();
     if (rcmp(rkk, tol) <= 0) {
       ok = false;
       break;
     }
     const R rinv = rdiv(rfrom<R>(1.0), rkk);  // every lane computes the same value
     if (lane == 0) RM.st(k + rk, cx<R>{rkk, rfrom<R>(0.0)});
-    for (int r = lane; r < n; r += 32) {
+    for (int r = lane; r < n; r += G) {
       const cx<R> q = cmulr(Q.ld(k * n + r), rinv);
       Q.st(k * n + r, q);
       PS.st(r, 0, cmul(cconj(q), BS.ld(r, 0)));
     }
-    __syncwarp();
+    g.sync();
     if (lane < 2) {  // y_k = <q_k, b> (linalg.hpp:117), real / imaginary part
       R y = rfrom<R>(0.0);
       for (int r = 0; r < n; ++r) y = radd(y, PS.ldr(2 * r + lane, 0));
@@ -1512,40 +1541,40 @@ __global__ void __launch_bounds__(128) lsq_coop(const TrackArgs a) {
     }
     // right-looking first pass: q_k projected out of every later column, one lane per column
     // (R(k,j) = 0 + r as the reference's out.r.at(i, k) += rik on a zero matrix)
-    for (int j = k + 1 + lane; j < n; j += 32) {
+    for (int j = k + 1 + lane; j < n; j += G) {
       cx<R> r = zero;
       for (int row = 0; row < n; ++row) r = cadd(r, cmul(cconj(Q.ld(k * n + row)), Q.ld(j * n + row)));
       RM.st(k + j * (j + 1) / 2, cadd(zero, r));
       for (int row = 0; row < n; ++row) Q.st(j * n + row, csub(Q.ld(j * n + row), cmul(r, Q.ld(k * n + row))));
     }
-    __syncwarp();
+    g.sync();
   }
   if (lane == 0) si(F_OK, s) = ok ? 1 : 0;
   if (!ok) return;
   // back substitution R x = y (linalg.hpp:118-122): products by the lanes, sums in order by lanes 0/1
   for (int j = n - 1; j >= 0; --j) {
-    for (int i = j + 1 + lane; i < n; i += 32) PS.st(i, 0, cmul(RM.ld(j + i * (i + 1) / 2), DS.ld(i, 0)));
-    __syncwarp();
+    for (int i = j + 1 + lane; i < n; i += G) PS.st(i, 0, cmul(RM.ld(j + i * (i + 1) / 2), DS.ld(i, 0)));
+    g.sync();
     if (lane < 2) {  // real / imaginary part of acc -= R_ji x_i, in order
       R acc = YS.ldr(2 * j + lane, 0);
       for (int i = j + 1; i < n; ++i) acc = rsub(acc, PS.ldr(2 * i + lane, 0));
       PS.str(lane, 0, acc);
     }
-    __syncwarp();
+    g.sync();
     if (lane == 0) DS.st(j, 0, cdiv(PS.ld(0, 0), RM.ld(j + j * (j + 1) / 2)));
-    __syncwarp();
+    g.sync();
   }
   // x += dx; update and iterate norms (tracker.cpp:258-264)
   double dxn = 0.0, xn = 0.0;
-  for (int v = lane; v < n; v += 32) {
+  for (int v = lane; v < n; v += G) {
     const cx<R> dv = DS.ld(v, 0);
     const cx<R> xv = cadd(X.ld(v, s), dv);
     X.st(v, s, xv);
     dxn = f_max(dxn, cabsd(dv));
     xn = f_max(xn, cabsd(xv));
   }
-  dxn = warp_fmax(dxn);
-  xn = warp_fmax(xn);
+  dxn = g.fmax(dxn);
+  xn = g.fmax(xn);
   if (lane == 0) {
     a.sd[D_DXN * a.S + s] = dxn;
     a.sd[D_XN * a.S + s] = xn;
@@ -1599,9 +1628,15 @@ __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
    reinterpret_cast<const void*>(&pp::dev::step_trip<R>),                             \
    reinterpret_cast<const void*>(&pp::dev::eval_kernel<R, KM>),                       \
    reinterpret_cast<const void*>(&pp::dev::lsq_kernel<R>),                            \
-   reinterpret_cast<const void*>(&pp::dev::eval_coop<R, KM>),                         \
-   reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, false>),                       \
-   reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, true>),                        \
+   {reinterpret_cast<const void*>(&pp::dev::eval_coop<R, KM, 32>),                    \
+    reinterpret_cast<const void*>(&pp::dev::eval_coop<R, KM, 8>),                     \
+    reinterpret_cast<const void*>(&pp::dev::eval_coop<R, KM, 4>)},                    \
+   {reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, false, 32>),                  \
+    reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, false, 8>),                   \
+    reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, false, 4>)},                  \
+   {reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, true, 32>),                   \
+    reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, true, 8>),                    \
+    reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, true, 4>)},                   \
    reinterpret_cast<const void*>(&pp::dev::ctrl_eval_trip<R, KM, true, (sizeof(R) < 32 ? 4 : 1)>),             \
    reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, true, 256, 2>),                                        \
    reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, false, 128, PP_LSQ_MINB, true>)}

@@ -22,7 +22,10 @@
 // quad-double operations are 100-250 binary64 instructions each; they are real calls on the
 // device so that kernels built from them stay compact (code size, compile time, I-cache)
 #define PP_QD_FN static __host__ __device__ __noinline__
+// the bodies of the hot quad-double operations, inlined into the complex operations below
+#define PP_QD_INL static __host__ __device__ __forceinline__
 #else
+#define PP_QD_INL inline
 #define PP_HD inline
 #define PP_QD_FN inline
 #define PP_UNROLL
@@ -239,7 +242,7 @@ PP_HD qd_t renorm(double c0, double c1, double c2, double c3) {
 }
 
 // 5-limb renormalisation (xprec.hpp:107-155)
-PP_QD_FN qd_t renorm(double c0, double c1, double c2, double c3, double c4) {
+PP_QD_INL qd_t renorm5_i(double c0, double c1, double c2, double c3, double c4) {
   if (f_isinf(c0)) return qd_t{c0, c1, c2, c3};
   double s0, s1, s2 = 0.0, s3 = 0.0;
   s0 = quick_two_sum(c3, c4, c4);
@@ -281,6 +284,7 @@ PP_QD_FN qd_t renorm(double c0, double c1, double c2, double c3, double c4) {
   }
   return qd_t{s0, s1, s2, s3};
 }
+PP_QD_FN qd_t renorm(double c0, double c1, double c2, double c3, double c4) { return renorm5_i(c0, c1, c2, c3, c4); }
 
 // merge step of the accurate addition (xprec.hpp:158-173); returns (emit, s)
 PP_HD double three_accum(double& a, double& b, double c) {
@@ -333,7 +337,8 @@ PP_HD void put(double& x0, double& x1, double& x2, double& x3, int k, double s) 
 PP_HD qd_t rneg(qd_t a) { return qd_t{-a.c0, -a.c1, -a.c2, -a.c3}; }
 
 // accurate merge-based addition (xprec.hpp:325-382)
-PP_QD_FN qd_t radd(qd_t a, qd_t b) {
+namespace qdi {
+PP_QD_INL qd_t add_i(qd_t a, qd_t b) {
   qdi::LimbQueue qa{a.c0, a.c1, a.c2, a.c3, 4};
   qdi::LimbQueue qb{b.c0, b.c1, b.c2, b.c3, 4};
   double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0, x4 = 0.0;
@@ -365,8 +370,10 @@ PP_UNROLL
     else
       x4 = v;
   }
-  return qdi::renorm(x0, x1, x2, x3, x4);
+  return qdi::renorm5_i(x0, x1, x2, x3, x4);
 }
+}  // namespace qdi
+PP_QD_FN qd_t radd(qd_t a, qd_t b) { return qdi::add_i(a, b); }
 
 PP_QD_FN qd_t radd(qd_t a, double b) {
   double e;
@@ -395,7 +402,8 @@ PP_QD_FN qd_t rmuld(qd_t a, double b) {
 }
 
 // symmetric accurate product (xprec.hpp:420-480)
-PP_QD_FN qd_t rmul(qd_t a, qd_t b) {
+namespace qdi {
+PP_QD_INL qd_t mul_i(qd_t a, qd_t b) {
   double q0;
   double p0 = two_prod(a.c0, b.c0, q0);
 
@@ -452,8 +460,10 @@ PP_QD_FN qd_t rmul(qd_t a, qd_t b) {
   acc = f_add(acc, f_add(f_add(q22e, cr3e), cr4e));
   acc = f_add(acc, f_add(f_add(xe3, ye3), f_add(xe4, ye4)));
   acc = f_add(acc, f_add(f_add(f_mul(a.c1, b.c3), f_mul(a.c3, b.c1)), f_mul(a.c2, b.c2)));
-  return qdi::renorm(p0, h1, s2, s3, acc);
+  return qdi::renorm5_i(p0, h1, s2, s3, acc);
 }
+}  // namespace qdi
+PP_QD_FN qd_t rmul(qd_t a, qd_t b) { return qdi::mul_i(a, b); }
 
 PP_QD_FN qd_t rdiv(qd_t a, qd_t b) {
   double q0 = f_div(a.c0, b.c0);
@@ -635,6 +645,20 @@ template <class R>
 PP_HD double cabsd(cx<R> a) {
   return rtod(cabsr(a));
 }
+// complex quad-double: one call per complex operation, with the real operations inlined inside it,
+// so that the independent real products and sums of a complex operation are scheduled together
+// (the same operations in the same order as the templates above; exact-match overloads win)
+PP_QD_FN cx<qd_t> cmul(cx<qd_t> a, cx<qd_t> b) {
+  return cx<qd_t>{qdi::add_i(qdi::mul_i(a.re, b.re), rneg(qdi::mul_i(a.im, b.im))),
+                  qdi::add_i(qdi::mul_i(a.re, b.im), qdi::mul_i(a.im, b.re))};
+}
+PP_QD_FN cx<qd_t> cadd(cx<qd_t> a, cx<qd_t> b) { return cx<qd_t>{qdi::add_i(a.re, b.re), qdi::add_i(a.im, b.im)}; }
+PP_QD_FN cx<qd_t> csub(cx<qd_t> a, cx<qd_t> b) {
+  return cx<qd_t>{qdi::add_i(a.re, rneg(b.re)), qdi::add_i(a.im, rneg(b.im))};
+}
+PP_QD_FN cx<qd_t> cmulr(cx<qd_t> a, qd_t s) { return cx<qd_t>{qdi::mul_i(a.re, s), qdi::mul_i(a.im, s)}; }
+PP_QD_FN qd_t cabs2(cx<qd_t> a) { return qdi::add_i(qdi::mul_i(a.re, a.re), qdi::mul_i(a.im, a.im)); }
+
 // Smith division (complex.hpp:92-107); b != 0 is the caller's invariant
 template <class R>
 PP_HD cx<R> cdiv(cx<R> a, cx<R> b) {
