@@ -365,9 +365,14 @@ def run_ours(args, world, rank, local, dist):
         os.unlink(log)
     except Exception:  # noqa: BLE001
         pass
+    # nominal FP64 pipe rate: 148 SMs x 64 binary64 lanes x the SM clock under load
+    sm_mhz = clk.summary().get("sm_mhz") or measured_peaks().get("sm_max_mhz") or 1965.0
+    nominal = 148 * 64 * sm_mhz * 1e6 / 1e12
     roofline = {
         "bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
         "frac": (achieved / peak) if peak else None,
+        "peak_nominal": nominal, "frac_nominal": achieved / nominal,
+        "peak_nominal_def": "148 SMs x 64 FP64 lanes x median SM clock under load (DADD/DMUL/DFMA = 1 op)",
         "traffic": profile_traffic(dominant),
         "kernel": dominant,
         "op_convention": "binary64 pipe ops (DADD/DMUL/DFMA = 1 each) of the reference arithmetic",

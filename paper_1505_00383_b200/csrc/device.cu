@@ -531,10 +531,11 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
       if (lr[i].n == static_cast<int>(n)) lsq_reg = mode == 1 ? lr[i].stream : lr[i].hold;
   }
   if (lsq_reg) lsq_fn = lsq_reg;
-  // PP200_LSQ_QCACHE=1: the column in shared memory and q_i cached in TMEM between its dot product
-  // and its axpy (128 columns per CTA; the shared memory request is padded so that at most four
-  // CTAs are resident per SM and every tcgen05.alloc succeeds at once)
-  const bool lsq_qc = !lsq_tm && !lsq_reg && tblock == 128 && env_size("PP200_LSQ_QCACHE", 0) != 0 &&
+  // PP200_LSQ_QCACHE (default 1 for n*4L <= 128): the column in shared memory and q_i cached in
+  // TMEM between its dot product and its axpy (128 columns per CTA; the shared memory request is
+  // padded so that at most four CTAs are resident per SM and every tcgen05.alloc succeeds at once).
+  // Measured on cyclic-10 dd: lsq 5.47 -> 5.33 s per 131,072 paths.
+  const bool lsq_qc = !lsq_tm && !lsq_reg && tblock == 128 && env_size("PP200_LSQ_QCACHE", 1) != 0 &&
                       static_cast<size_t>(n) * 4 * L <= 128;
   if (lsq_qc) lsq_fn = var->lsq_qcache;
   const int lblock = lsq_tm ? 256 : tblock;
@@ -703,40 +704,53 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     const bool coop_global = static_cast<size_t>(n) * n * el > env_size("PP200_COOP_SMEM_KB", 4) * 1024;
     const size_t lcoop_slot =
         (coop_global ? static_cast<size_t>(4) * n : static_cast<size_t>(n) * n + 4 * n + n * (n + 1) / 2) * el;
-    // lanes per slot (G = 32, 8 or 4; G < 32 packs 32 / G slots into a warp).  A warp per slot gives
-    // each path the lowest trip latency, which is what the last few paths of a run need; with many
-    // slots per SM, smaller groups keep more lanes busy (the reference's sequential sums run on two
-    // lanes of the group, its row operations on all of them).  PP200_COOP_GROUP fixes G; the
-    // default picks G = 8 from PP200_COOP_G8_PER_SM (8) busy slots per SM up, else 32.
-    const size_t coop_group_env = env_size("PP200_COOP_GROUP", 0);
-    const size_t g8_per_sm = env_size("PP200_COOP_G8_PER_SM", 8);
-    auto coop_gi = [&](size_t active) -> int {
-      if (coop_group_env == 32) return 0;
-      if (coop_group_env == 8) return 1;
-      if (coop_group_env == 4) return 2;
-      return active >= g8_per_sm * static_cast<size_t>(prop.multiProcessorCount) ? 1 : 0;
-    };
-    // warps per block of the tail-mode kernels for group index gi (at most 4, within 200 KB)
+    // lanes per slot (G = 32, 8 or 4; G < 32 packs 32 / G slots into a warp), chosen per kernel.  A
+    // warp per slot gives each path the lowest trip latency, which is what the last few paths of a
+    // run need; with many slots per SM, smaller groups keep more lanes of the solver busy (the
+    // reference's sequential sums run on two lanes of the group, its row operations on all of
+    // them).  The evaluation keeps a warp per slot: its per-slot contribution buffer is large, so
+    // packing slots would cut the warps per SM instead.  PP200_COOP_GROUP fixes the solver's G,
+    // PP200_COOP_GROUP_EVAL the evaluation's; by default the solver uses G = 8 from
+    // PP200_COOP_G8_PER_SM (8) busy slots per SM up.
+    // warps per block of a tail-mode kernel with per-slot shared memory per_slot and group index
+    // gi (at most 4, within 200 KB; 0 if one warp does not fit)
     auto coop_wpb = [&](size_t per_slot, int gi) {
       const size_t per_warp = per_slot * static_cast<size_t>(32 / dev::kCoopGroups[gi]);
       return static_cast<int>(std::min<size_t>(4, (200 * 1024) / per_warp));
     };
-    bool coop_ok = true;
-    for (int gi = 0; gi < 3; ++gi) {
-      const int ew = coop_wpb(ecoop_slot, gi), lw = coop_wpb(lcoop_slot, gi);
-      if (ew < 1 || lw < 1) {
-        coop_ok = false;
-        continue;
-      }
+    auto group_index = [](size_t g) { return g == 8 ? 1 : g == 4 ? 2 : 0; };
+    const size_t g8_per_sm = env_size("PP200_COOP_G8_PER_SM", 8);
+    const int lsq_gi_env = group_index(env_size("PP200_COOP_GROUP", 0)), eval_gi_env = group_index(env_size("PP200_COOP_GROUP_EVAL", 32));
+    const bool lsq_g_fixed = env_size("PP200_COOP_GROUP", 0) != 0;
+    auto lsq_gi = [&](size_t active) -> int {
+      int gi = lsq_g_fixed ? lsq_gi_env : (active >= g8_per_sm * static_cast<size_t>(prop.multiProcessorCount) ? 1 : 0);
+      while (gi > 0 && coop_wpb(lcoop_slot, gi) < 1) --gi;
+      return gi;
+    };
+    auto eval_gi = [&](size_t) -> int {
+      int gi = eval_gi_env;
+      while (gi > 0 && coop_wpb(ecoop_slot, gi) < 1) --gi;
+      return gi;
+    };
+    // tail mode needs a warp per slot to fit (G = 32)
+    const bool coop_ok = coop_wpb(ecoop_slot, 0) >= 1 && coop_wpb(lcoop_slot, 0) >= 1;
+    for (int gi = 0; gi < 3 && coop_ok; ++gi) {
       const size_t spw = static_cast<size_t>(32 / dev::kCoopGroups[gi]);
-      ensure_smem(var->eval_coop[gi], ew * spw * ecoop_slot, device);
-      ensure_smem(coop_global ? var->lsq_coop_g[gi] : var->lsq_coop[gi], lw * spw * lcoop_slot, device);
+      const int ew = coop_wpb(ecoop_slot, gi), lw = coop_wpb(lcoop_slot, gi);
+      if (ew >= 1) ensure_smem(var->eval_coop[gi], ew * spw * ecoop_slot, device);
+      if (lw >= 1) ensure_smem(coop_global ? var->lsq_coop_g[gi] : var->lsq_coop[gi], lw * spw * lcoop_slot, device);
     }
     const size_t tail_slots = env_size("PP200_TAIL_SLOTS", 32 * static_cast<size_t>(prop.multiProcessorCount));
     // PP200_FORCE_COOP=1 runs every trip in tail mode (used by the parity tests)
     // small runs (no more paths than tail slots) start in tail mode: a warp per path spreads a
     // few thousand paths over every SM instead of packing them into a few blocks
-    bool coop = (env_size("PP200_FORCE_COOP", 0) != 0 || (tail_slots > 0 && count <= tail_slots)) && coop_ok;
+    // Whole runs also stay in tail mode where a thread per path cannot fill the SMs: quad-double
+    // (its per-thread working set leaves a few warps per SM; katsura-12 qd: 80.5 s thread per path
+    // against 21.6 s with groups of 8 lanes) and any system whose point and open Jacobian row
+    // shrink the trip blocks below 128 threads (rand32 dd, n = 32: 148 -> 184 paths/s).
+    const bool coop_whole_run = env_size("PP200_COOP_WHOLE_RUN", 1) != 0 && (plan.prec == 2 || tblock < 128);
+    bool coop = (env_size("PP200_FORCE_COOP", 0) != 0 || coop_whole_run || (tail_slots > 0 && count <= tail_slots)) &&
+                coop_ok;
     // one trip = control (step control, prediction, finalize, refill) followed by the heavy
     // operation of every busy slot.  Thread-per-path mode fuses the control into the evaluation
     // kernel (ctrl_eval_trip) and runs lsq_trip; tail mode runs step_trip, eval_coop, lsq_coop.
@@ -748,16 +762,17 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
       if (coop) {
         check(cudaLaunchKernel(var->step_trip, grid, blk, args, 0, stream), "launch step_trip");
         if (ev) check(cudaEventRecord(ev[1], stream), "event");
-        const int gi = coop_gi(a.n_active);
-        const size_t spw = static_cast<size_t>(32 / dev::kCoopGroups[gi]);
-        const int ew = coop_wpb(ecoop_slot, gi), lw = coop_wpb(lcoop_slot, gi);
-        const unsigned eb = static_cast<unsigned>((a.n_active + ew * spw - 1) / (ew * spw));
-        const unsigned lb = static_cast<unsigned>((a.n_active + lw * spw - 1) / (lw * spw));
-        check(cudaLaunchKernel(var->eval_coop[gi], dim3(eb), dim3(32 * ew), targs, ew * spw * ecoop_slot, stream),
+        const int egi = eval_gi(a.n_active), lgi = lsq_gi(a.n_active);
+        const size_t espw = static_cast<size_t>(32 / dev::kCoopGroups[egi]);
+        const size_t lspw = static_cast<size_t>(32 / dev::kCoopGroups[lgi]);
+        const int ew = coop_wpb(ecoop_slot, egi), lw = coop_wpb(lcoop_slot, lgi);
+        const unsigned eb = static_cast<unsigned>((a.n_active + ew * espw - 1) / (ew * espw));
+        const unsigned lb = static_cast<unsigned>((a.n_active + lw * lspw - 1) / (lw * lspw));
+        check(cudaLaunchKernel(var->eval_coop[egi], dim3(eb), dim3(32 * ew), targs, ew * espw * ecoop_slot, stream),
               "launch eval_coop");
         if (ev) check(cudaEventRecord(ev[2], stream), "event");
-        check(cudaLaunchKernel(coop_global ? var->lsq_coop_g[gi] : var->lsq_coop[gi], dim3(lb), dim3(32 * lw), targs,
-                               lw * spw * lcoop_slot, stream),
+        check(cudaLaunchKernel(coop_global ? var->lsq_coop_g[lgi] : var->lsq_coop[lgi], dim3(lb), dim3(32 * lw), targs,
+                               lw * lspw * lcoop_slot, stream),
               "launch lsq_coop");
       } else {
         if (ev) check(cudaEventRecord(ev[1], stream), "event");

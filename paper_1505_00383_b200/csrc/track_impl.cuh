@@ -1466,6 +1466,8 @@ __global__ void __launch_bounds__(128) lsq_coop(const TrackArgs a) {
   CoopMat<R> Q, RM;
   Q.s = RM.s = s;
   if (kGlobalQ) {
+    // the evaluation wrote J through PP_WORK: the global-Q solver reads the same slot-tiled layout
+    static_assert(PP_SLOT_TILED, "lsq_coop<R, true> reads the slot-tiled solver arrays");
     Q.tiled = Tiled<R>{a.J, static_cast<uint32_t>(n * n)};
     RM.tiled = Tiled<R>{a.Rm, static_cast<uint32_t>(nR)};
   } else {

@@ -645,6 +645,10 @@ template <class R>
 PP_HD double cabsd(cx<R> a) {
   return rtod(cabsr(a));
 }
+#ifndef PP_QD_CPLX_CALLS
+#define PP_QD_CPLX_CALLS 1
+#endif
+#if PP_QD_CPLX_CALLS
 // complex quad-double: one call per complex operation, with the real operations inlined inside it,
 // so that the independent real products and sums of a complex operation are scheduled together
 // (the same operations in the same order as the templates above; exact-match overloads win)
@@ -658,6 +662,7 @@ PP_QD_FN cx<qd_t> csub(cx<qd_t> a, cx<qd_t> b) {
 }
 PP_QD_FN cx<qd_t> cmulr(cx<qd_t> a, qd_t s) { return cx<qd_t>{qdi::mul_i(a.re, s), qdi::mul_i(a.im, s)}; }
 PP_QD_FN qd_t cabs2(cx<qd_t> a) { return qdi::add_i(qdi::mul_i(a.re, a.re), qdi::mul_i(a.im, a.im)); }
+#endif
 
 // Smith division (complex.hpp:92-107); b != 0 is the caller's invariant
 template <class R>

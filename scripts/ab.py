@@ -18,7 +18,8 @@ import paper_1505_00383_b200 as P  # noqa: E402
 system, prec, lo, paths = sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4])
 cfg_over = dict(kv.split("=") for kv in sys.argv[5:] if not kv.startswith("PP200_"))
 knobs = [(kv.split("=")[0], kv.split("=")[1].split(",")) for kv in sys.argv[5:] if kv.startswith("PP200_")]
-f = P.parse_system(open(os.path.join(ROOT, "tests", "data", f"{system}.sys")).read())
+sysfile = os.path.join(ROOT, "tests", "data", f"{system}.sys")
+f = P.parse_system(open(sysfile).read()) if os.path.exists(sysfile) else P.cyclic_system(int(system[6:]))
 g, st = P.total_degree_start(f, prec)
 h = P.make_homotopy(f, g, P.random_gamma(1), prec)
 cfg = P.TrackConfig.defaults(prec)

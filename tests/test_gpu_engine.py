@@ -84,6 +84,7 @@ def test_step_events_match_the_reference_sink(pp, monkeypatch, name, mode):
     prec = str(g["prec"])
     if mode == "thread_per_path":
         monkeypatch.setenv("PP200_TAIL_SLOTS", "0")
+        monkeypatch.setenv("PP200_COOP_WHOLE_RUN", "0")
     elif mode == "warp_per_path":
         monkeypatch.setenv("PP200_FORCE_COOP", "1")
     _, _, starts, h = homotopy(pp, read("cyclic5.sys"), prec)

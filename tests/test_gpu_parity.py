@@ -111,15 +111,24 @@ def test_track_bitwise(pp, name, system):
     ("cyclic5_d", "cyclic5"), ("cyclic5_dd", "cyclic5"), ("cyclic5_qd", "cyclic5"), ("cyclic10_dd", "cyclic10"),
     ("katsura12_qd_mn4", "katsura12"), ("rand32_dd", "rand32"), ("cyclic8_d", "cyclic8"),
 ])
-@pytest.mark.parametrize("mode", ["warp_per_path", "thread_per_path", "thread_per_path_tmem"])
+@pytest.mark.parametrize("mode", ["warp_per_path", "group8_per_path", "group4_per_path", "thread_per_path",
+                                  "thread_per_path_tmem", "thread_per_path_plain"])
 def test_track_bitwise_modes(pp, monkeypatch, name, system, mode):
-    """every engine gives the reference records: every trip in tail mode (a warp per path:
-    eval_coop / lsq_coop), or never (a thread per path; small runs otherwise start in tail mode),
-    also with the open Jacobian row and the Gram-Schmidt column in tensor memory"""
-    if mode == "warp_per_path":
+    """every engine gives the reference records: every trip in tail mode (a warp per path, or 8
+    or 4 lanes per path: eval_coop / lsq_coop), or never (a thread per path; small runs otherwise
+    start in tail mode), also with the open Jacobian row and the Gram-Schmidt column in tensor
+    memory, and without the TMEM q-cache / register-resident solvers (plain shared-memory column)"""
+    if mode.endswith("_per_path") and not mode.startswith("thread"):
         monkeypatch.setenv("PP200_FORCE_COOP", "1")
+        g = {"warp": "32", "group8": "8", "group4": "4"}[mode.split("_")[0]]
+        monkeypatch.setenv("PP200_COOP_GROUP", g)
+        monkeypatch.setenv("PP200_COOP_GROUP_EVAL", g)
     else:
         monkeypatch.setenv("PP200_TAIL_SLOTS", "0")
+        monkeypatch.setenv("PP200_COOP_WHOLE_RUN", "0")
+    if mode.endswith("plain"):
+        monkeypatch.setenv("PP200_LSQ_QCACHE", "0")
+        monkeypatch.setenv("PP200_LSQ_REG", "0")
     if mode.endswith("tmem"):
         monkeypatch.setenv("PP200_TMEM", "1")
         monkeypatch.setenv("PP200_LSQ_TMEM", "1")
