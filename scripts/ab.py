@@ -40,7 +40,9 @@ def bits(a):
 
 
 ref = None
-os.environ["PP200_KERNEL_TIMING"] = "1"
+# per-kernel times need the instrumented engine (one launch per kernel and trip, synchronised);
+# AB_TIMING=0 times the production engine (CUDA graphs) as a whole instead
+os.environ["PP200_KERNEL_TIMING"] = os.environ.get("AB_TIMING", "1")
 for combo in itertools.product(*[v for _, v in knobs]):
     for (k, _), v in zip(knobs, combo):
         os.environ[k] = v
@@ -51,5 +53,6 @@ for combo in itertools.product(*[v for _, v in knobs]):
     gok = {name: all(np.array_equal(bits(getattr(sol, k)[int(z["lo"]) - lo:int(z["hi"]) - lo]), bits(z[k])) for k in KEYS)
            for name, z in golds}
     print(f"{dict(zip([k for k, _ in knobs], combo))} {system} {prec} {paths}: device {s['device_ms']:.1f} ms "
-          f"eval {s['eval_ms']:.1f} lsq {s['lsq_ms']:.1f} step {s['step_ms']:.1f} trips {s['total_rounds']} "
+          f"eval {s['eval_ms']:.1f} lsq {s['lsq_ms']:.1f} step {s['step_ms']:.1f} fused {s.get('fused_ms', 0):.1f} "
+          f"trips {s['total_rounds']} "
           f"-> {paths / (s['device_ms'] / 1e3):.1f} paths/s; same-as-first {same} golden {gok}", flush=True)

@@ -27,11 +27,14 @@ def assert_golden_ranges(sol, g, call_lo):
         assert np.array_equal(sol.path_id[off:off + per], g["path_id"][i * per:(i + 1) * per])
 
 
-@pytest.mark.parametrize("name", ["cyclic10_dd_prod", "cyclic10_d_prod"])
-def test_production_occupancy_bitwise(pp, name):
+@pytest.mark.parametrize("name,fused", [("cyclic10_dd_prod", None), ("cyclic10_d_prod", None),
+                                        ("cyclic10_dd_prod", "1"), ("cyclic10_dd_prod", "0")])
+def test_production_occupancy_bitwise(pp, monkeypatch, name, fused):
     """BASELINE config 3 at the bench's size: cyclic-10 dd over 262,144 paths (592 blocks of 128
     slots, open row in TMEM, 16-trip graphs, compaction, tail mode); cyclic-10 d over 524,288 paths
     (1,024 slots per SM, register-resident solver)"""
+    if fused is not None:  # None: the default engine; "1" / "0": with and without the fused trip kernel
+        monkeypatch.setenv("PP200_FUSED", fused)
     g = golden(f"track_{name}")
     prec = str(g["prec"])
     _, _, starts, h = homotopy(pp, read("cyclic10.sys"), prec)
@@ -78,13 +81,14 @@ def per_path(ev):
 
 
 @pytest.mark.parametrize("name", ["cyclic5_d", "cyclic5_dd", "cyclic5_d_tight"])
-@pytest.mark.parametrize("mode", ["default", "thread_per_path", "warp_per_path"])
+@pytest.mark.parametrize("mode", ["default", "thread_per_path", "thread_per_path_fused", "warp_per_path"])
 def test_step_events_match_the_reference_sink(pp, monkeypatch, name, mode):
     g = golden(f"events_{name}")
     prec = str(g["prec"])
-    if mode == "thread_per_path":
+    if mode.startswith("thread_per_path"):
         monkeypatch.setenv("PP200_TAIL_SLOTS", "0")
         monkeypatch.setenv("PP200_COOP_WHOLE_RUN", "0")
+        monkeypatch.setenv("PP200_FUSED", "1" if mode.endswith("fused") else "0")
     elif mode == "warp_per_path":
         monkeypatch.setenv("PP200_FORCE_COOP", "1")
     _, _, starts, h = homotopy(pp, read("cyclic5.sys"), prec)
