@@ -344,63 +344,39 @@ def run_ours(args, world, rank, local, dist):
         os.environ.pop("PP200_TRIP_LOG", None)
     sti = sol_i.stats
     work = W.path_work(info, PREC, sti["evals"], sti["solves"])
-    fused_ms = sti.get("fused_ms", 0.0)
+    lsq_rate = work["lsq_total"] / (sti["lsq_ms"] / 1e3)
+    eval_rate = work["eval_total"] / (sti["eval_ms"] / 1e3)
+    dominant = "lsq_trip" if sti["lsq_ms"] >= sti["eval_ms"] else "ctrl_eval_trip"
+    achieved = (lsq_rate if dominant == "lsq_trip" else eval_rate) / 1e12
     peak_ops = fp64_peak_ops(local)
     peak = peak_ops / 1e12 if peak_ops else None
-    tot_ms = max(1e-9, sti["eval_ms"] + sti["lsq_ms"] + sti["step_ms"] + fused_ms)
-    if fused_ms > 0:
-        # thread-per-path trips run as one fused kernel (control + evaluation + solve); the tail-mode
-        # kernels (step_trip, eval_coop, lsq_coop) run the last paths.  The fused kernel dominates:
-        # its ops are those of the evaluations and solves it performed (all but the tail's).
-        dominant = "trips_fused"
-        achieved = None  # filled from the steady-state trips below when available
-        fused_rate = None
-        shares = {"trips_fused (control + evaluation + solve)": fused_ms / tot_ms,
-                  "tail mode evaluation (eval_coop)": sti["eval_ms"] / tot_ms,
-                  "tail mode solve (lsq_coop)": sti["lsq_ms"] / tot_ms,
-                  "tail mode control (step_trip)": sti["step_ms"] / tot_ms}
-        lsq_rate = eval_rate = None
-    else:
-        lsq_rate = work["lsq_total"] / (sti["lsq_ms"] / 1e3)
-        eval_rate = work["eval_total"] / (sti["eval_ms"] / 1e3)
-        dominant = "lsq_trip" if sti["lsq_ms"] >= sti["eval_ms"] else "ctrl_eval_trip"
-        achieved = (lsq_rate if dominant == "lsq_trip" else eval_rate) / 1e12
-        shares = {"ctrl_eval_trip (control + evaluation)": sti["eval_ms"] / tot_ms, "lsq_trip": sti["lsq_ms"] / tot_ms,
-                  "tail mode control (step_trip)": sti["step_ms"] / tot_ms}
+    tot_ms = max(1e-9, sti["eval_ms"] + sti["lsq_ms"] + sti["step_ms"])
+    shares = {"ctrl_eval_trip (control + evaluation)": sti["eval_ms"] / tot_ms, "lsq_trip": sti["lsq_ms"] / tot_ms,
+              "tail mode control (step_trip)": sti["step_ms"] / tot_ms}
     steady = None
     try:
         t = np.loadtxt(log, ndmin=2)
         full = (t[:, 1] >= t[:, 5]) & (t[:, 6] == 0)  # thread-per-path trips on which every slot was busy
-        thread = t[:, 6] == 0
-        if fused_ms > 0 and thread.any():
-            # ops of the fused kernel's trips: every busy slot evaluated once and (most) solved once;
-            # the evaluations / solves of the tail-mode trips are taken out by their share of busy slots
-            busy_thread = t[thread, 1].sum()
-            share = busy_thread / max(1.0, t[:, 1].sum())
-            ops_fused = share * (work["eval_total"] + work["lsq_total"])
-            fused_rate = ops_fused / (fused_ms / 1e3)
-            achieved = fused_rate / 1e12
         if full.any() and peak_ops:
-            if fused_ms > 0:
-                steady = {"trips": int(full.sum()), "of_trips": len(t),
-                          "fused_frac": float((t[full, 1] * (work["eval_ops"] + work["lsq_ops"])).sum()
-                                              / (t[full, 2].sum() / 1e3) / peak_ops),
-                          "busy_weighted_slot_use": float(t[:, 1].sum() / t[:, 5].sum())}
-            else:
-                steady = {"trips": int(full.sum()), "of_trips": len(t),
-                          "eval_frac": float((t[full, 1] * work["eval_ops"]).sum() / (t[full, 2].sum() / 1e3) / peak_ops),
-                          "lsq_frac": float((t[full, 1] * work["lsq_ops"]).sum() / (t[full, 3].sum() / 1e3) / peak_ops),
-                          "busy_weighted_slot_use": float(t[:, 1].sum() / t[:, 5].sum())}
+            steady = {"trips": int(full.sum()), "of_trips": len(t),
+                      "eval_frac": float((t[full, 1] * work["eval_ops"]).sum() / (t[full, 2].sum() / 1e3) / peak_ops),
+                      "lsq_frac": float((t[full, 1] * work["lsq_ops"]).sum() / (t[full, 3].sum() / 1e3) / peak_ops),
+                      "busy_weighted_slot_use": float(t[:, 1].sum() / t[:, 5].sum())}
         os.unlink(log)
     except Exception:  # noqa: BLE001
         pass
     # nominal FP64 pipe rate: 148 SMs x 64 binary64 lanes x the SM clock under load
     sm_mhz = clk.summary().get("sm_mhz") or measured_peaks().get("sm_max_mhz") or 1965.0
     nominal = 148 * 64 * sm_mhz * 1e6 / 1e12
+    # nominal FP64 pipe rate: 148 SMs x 64 binary64 lanes x the SM clock under load
+    sm_mhz = clk.summary().get("sm_mhz") or measured_peaks().get("sm_max_mhz") or 1965.0
+    nominal = 148 * 64 * sm_mhz * 1e6 / 1e12
     roofline = {
         "bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-        "frac": (achieved / peak) if (peak and achieved) else None,
-        "peak_nominal": nominal, "frac_nominal": (achieved / nominal) if achieved else None,
+        "frac": (achieved / peak) if peak else None,
+        "peak_nominal": nominal, "frac_nominal": achieved / nominal,
+        "peak_nominal_def": "148 SMs x 64 FP64 lanes x median SM clock under load (DADD/DMUL/DFMA = 1 op)",
+        "peak_nominal": nominal, "frac_nominal": achieved / nominal,
         "peak_nominal_def": "148 SMs x 64 FP64 lanes x median SM clock under load (DADD/DMUL/DFMA = 1 op)",
         "traffic": profile_traffic(dominant),
         "kernel": dominant,
@@ -409,8 +385,7 @@ def run_ours(args, world, rank, local, dist):
                        "MEASURED_PEAKS.json has no FP64 figure",
         "achieved_def": "algorithmic ops of all launches of the kernel in one instrumented step / their summed "
                         "CUDA-event time (tail trips with few busy slots included)",
-        "ctrl_eval_trip_tflops": eval_rate / 1e12 if eval_rate else None,
-        "lsq_trip_tflops": lsq_rate / 1e12 if lsq_rate else None,
+        "ctrl_eval_trip_tflops": eval_rate / 1e12, "lsq_trip_tflops": lsq_rate / 1e12,
         "steady_state": steady,
         "kernel_time_share": shares,
         "ops_per_unit": {"eval": work["eval_ops"], "lsq": work["lsq_ops"]},

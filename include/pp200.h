@@ -113,7 +113,6 @@ typedef struct pp_run_stats {
   double lsq_ms;
   double step_ms;
   uint64_t events;       /* step events handed to the sink (pp_track_all_ex) */
-  double fused_ms;       /* PP200_KERNEL_TIMING: time of the fused trip kernel (evaluation + solve) */
 } pp_run_stats;
 
 typedef struct pp_system pp_system;     /* PolySystem (polysys.hpp:41-51) */

@@ -119,7 +119,6 @@ class RunStatsC(ctypes.Structure):
         ("lsq_ms", ctypes.c_double),
         ("step_ms", ctypes.c_double),
         ("events", ctypes.c_uint64),
-        ("fused_ms", ctypes.c_double),
     ]
 
 

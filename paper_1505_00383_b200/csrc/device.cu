@@ -543,15 +543,6 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   if (lsq_qc) lsq_smem = std::max<size_t>(lsq_smem, (prop.sharedMemPerMultiprocessor / 5) + 1024);
   ensure_smem(ctrl_eval_fn, eval_smem, device);
   ensure_smem(lsq_fn, lsq_smem, device);
-  // PP200_FUSED: trips of the thread-per-path mode as one kernel running K trips (trips_fused:
-  // control, evaluation with the open row in TMEM, solve with the TMEM q-cache); needs the TMEM
-  // evaluation and 128-thread trip blocks.  Shared memory is padded to at most four CTAs per SM
-  // (4 x 128 TMEM columns).
-  const bool fused = env_size("PP200_FUSED", 0) != 0 && tmem && tblock == 128 && eblock == 128 &&
-                     static_cast<size_t>(n) * 4 * L <= 128 && var->trips_fused != nullptr;
-  const size_t fused_smem = std::max<size_t>(static_cast<size_t>(tblock) * per_thread_smem,
-                                             prop.sharedMemPerMultiprocessor / 5 + 1024);
-  if (fused) ensure_smem(var->trips_fused, fused_smem, device);
   // slots: PP200_SLOTS_PER_SM per SM (default 512; 1024 in complex double, whose kernels are
   // memory-latency bound and want more warps), never more than the paths (whole blocks)
   const size_t per_sm = std::max<size_t>(tblock, env_size("PP200_SLOTS_PER_SM", L == 1 ? 1024 : 512));
@@ -694,7 +685,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   };
 
   uint64_t trips = 0, launches = 0, compactions = 0, per_graph_launches = 0;
-  float kms[4] = {0, 0, 0, 0};  // eval (thread mode: control + evaluation), lsq, tail control, fused trips
+  float kms[3] = {0, 0, 0};  // eval (thread mode: control + evaluation), lsq, tail-mode control
   a.n_active = S;
   a.tmem_cols = tmem_cols;
   {
@@ -765,22 +756,8 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     // kernel (ctrl_eval_trip) and runs lsq_trip; tail mode runs step_trip, eval_coop, lsq_coop.
     // The control part counts the slots with work in this trip into *busy_ptr.  With events
     // (instrumented mode) the three phases are bracketed: ev[0] ctrl ev[1] eval ev[2] lsq ev[3].
-    // K fused trips in one launch (thread-per-path mode with PP200_FUSED)
-    auto launch_fused = [&](unsigned* busy_ptr, int k) {
-      void* args[] = {&a, &busy_ptr, &k};
-      check(cudaLaunchKernel(var->trips_fused, grid, blk, args, fused_smem, stream), "launch trips_fused");
-      launches += 1;
-    };
     auto launch_trip = [&](unsigned* busy_ptr, cudaEvent_t* ev) {
       void* args[] = {&a, &busy_ptr};
-      if (fused && !coop) {
-        if (ev) check(cudaEventRecord(ev[0], stream), "event");
-        if (ev) check(cudaEventRecord(ev[1], stream), "event");
-        launch_fused(busy_ptr, 1);
-        if (ev) check(cudaEventRecord(ev[2], stream), "event");
-        if (ev) check(cudaEventRecord(ev[3], stream), "event");
-        return;
-      }
       if (ev) check(cudaEventRecord(ev[0], stream), "event");
       if (coop) {
         check(cudaLaunchKernel(var->step_trip, grid, blk, args, 0, stream), "launch step_trip");
@@ -864,13 +841,9 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
         const unsigned long long nbusy = *reinterpret_cast<unsigned*>(mbox);
         float tms[3] = {0, 0, 0};  // ctrl, eval (thread mode: control + evaluation), lsq
         for (int k = 0; k < 3; ++k) check(cudaEventElapsedTime(&tms[k], ev[k], ev[k + 1]), "event time");
-        if (fused && !trip_coop) {
-          kms[3] += tms[1];
-        } else {
-          kms[0] += tms[1];
-          kms[1] += tms[2];
-          kms[2] += tms[0];
-        }
+        kms[0] += tms[1];
+        kms[1] += tms[2];
+        kms[2] += tms[0];
         if (trip_log)
           std::fprintf(trip_log.get(), "%llu %llu %.4f %.4f %.4f %llu %d\n", static_cast<unsigned long long>(trips), nbusy,
                        tms[1], tms[2], tms[0], static_cast<unsigned long long>(trip_active), trip_coop ? 1 : 0);
@@ -889,11 +862,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
         capg.active = true;
         check(cudaMemsetAsync(busy, 0, graph_trips * sizeof(unsigned), stream), "memset busy");
         const uint64_t l0 = launches;
-        if (fused && !coop) {
-          launch_fused(busy, static_cast<int>(graph_trips));
-        } else {
-          for (size_t j = 0; j < graph_trips; ++j) launch_trip(busy + j, nullptr);
-        }
+        for (size_t j = 0; j < graph_trips; ++j) launch_trip(busy + j, nullptr);
         per_graph_launches = launches - l0;
         launches = l0;  // counted per graph launch below
         capg.active = false;
@@ -972,7 +941,6 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     stats->eval_ms = kms[0];
     stats->lsq_ms = kms[1];
     stats->step_ms = kms[2];
-    stats->fused_ms = kms[3];
     stats->events = n_events;
     stats->wall_ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();

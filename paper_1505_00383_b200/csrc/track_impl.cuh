@@ -1310,98 +1310,6 @@ __global__ void __launch_bounds__(128, kMinBlocks) ctrl_eval_trip(const TrackArg
 }
 
 // ---------------------------------------------------------------------------------------------
-// fused trips (thread per path): K trips of control + evaluation + least squares in one launch
-// ---------------------------------------------------------------------------------------------
-// Slots are independent, so nothing needs a grid-wide barrier between trips: each CTA runs its
-// 128 slots through K trips back to back.  Against one launch per kernel per trip this removes
-// 2K kernel boundaries, at each of which every SM waits for the slowest CTA of the launch (CTAs
-// differ in work: slots finalising, refilling or idle), and it keeps the CTA's TMEM allocation
-// and shared memory across trips.  Shared memory holds the point (x) and the Gram-Schmidt
-// column; TMEM (128 columns per CTA) holds the open Jacobian row during the evaluation and the
-// q_i cache during the solve.  The operation sequence of every slot is unchanged.
-template <class R, int KMAX>
-__global__ void __launch_bounds__(128, 4) trips_fused(const TrackArgs a, unsigned* busy_out, int ntrips) {
-  constexpr int L = level<R>::L;
-  extern __shared__ double smem[];
-  const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool in_range = s < a.n_active;
-  const int n = a.plan.n;
-  const size_t ls = threadIdx.x;
-  const Planar<R> XS{smem, blockDim.x};
-  const SmemRow<R> C{Planar<R>{smem + static_cast<size_t>(n) * 2 * L * blockDim.x, blockDim.x}, ls};
-  __shared__ uint32_t tmem_holder;
-  const uint32_t tbase = tmem_alloc_cta<128>(&tmem_holder);
-  const int warp = threadIdx.x >> 5;
-  const uint32_t quarter = tbase + (static_cast<uint32_t>(32 * (warp & 3)) << 16);
-  const SlotInts si{a.si, a.S};
-  const Planar<R> X{a.x, a.S}, SR{a.sr, a.S};
-  const auto J = PP_WORK(a.J, n * a.plan.n_polys), B = PP_WORK(a.B, a.plan.n_polys);
-  const auto JQ = PP_WORK(a.J, n * n), Rm = PP_WORK(a.Rm, n * (n + 1) / 2), BQ = PP_WORK(a.B, n),
-             Y = PP_WORK(a.Y, n);
-  for (int trip = 0; trip < ntrips; ++trip) {
-    // control, then the evaluation at the slot's point (ctrl_eval_trip)
-    int mode = M_DONE;
-    bool need = false;
-    R t = rfrom<R>(1.0);
-    if (in_range) {
-      mode = si(F_MODE, s);
-      if (mode != M_DONE) {
-        for (int v = 0; v < n; ++v) XS.st(v, ls, X.ld(v, s));
-        HeavyOut<R> ho;
-        ho.ok = si(F_OK, s) != 0;
-        ho.resid = a.sd[D_RESID * a.S + s];
-        ho.dxn = a.sd[D_DXN * a.S + s];
-        ho.xn = a.sd[D_XN * a.S + s];
-        ho.resid_r = SR.ldr(R_RESID, s);
-        mode = step_slot<R>(a, s, XS, ls, ho);
-        need = mode == M_NEWTON || mode == M_REFINE || mode == M_FINAL;
-        if (mode == M_NEWTON) t = SR.ldr(R_TNEXT, s);
-      }
-    }
-    if (__any_sync(0xffffffffu, need)) {
-      double resid;
-      R resid_r;
-      eval_hj<R, KMAX>(a.plan, XS, TmemRow<R>{quarter}, ls, t, B, J, s, resid, resid_r);
-      if (need) {
-        a.sd[D_RESID * a.S + s] = resid;
-        SR.str(R_RESID, s, resid_r);
-      }
-    }
-    const bool solve = mode == M_NEWTON || mode == M_REFINE;
-    const unsigned busy = __ballot_sync(0xffffffffu, in_range && mode != M_DONE);
-    const unsigned nsolve = __ballot_sync(0xffffffffu, in_range && solve);
-    if ((threadIdx.x & 31) == 0 && busy != 0) {
-      atomicAdd(busy_out + trip, static_cast<unsigned>(__popc(busy)));
-      atomicAdd(a.work, static_cast<unsigned long long>(__popc(busy)));
-      atomicAdd(a.work + 1, static_cast<unsigned long long>(__popc(nsolve)));
-    }
-    // the least-squares Newton update (lsq_trip, TMEM q-cache); the point is still in XS
-    if (nsolve != 0) {
-      const bool ok = lsq_solve_c<R, decltype(JQ), SmemRow<R>, true>(n, n, a.rank_tol, JQ, Rm, BQ, Y, s, C,
-                                                                      TmemQCache<R>{quarter});
-      if (solve) {
-        si(F_OK, s) = ok ? 1 : 0;
-        if (ok) {
-          double dxn = 0.0, xn = 0.0;
-          for (int v = 0; v < n; ++v) {
-            const cx<R> dv = C.ld(v);
-            const cx<R> xv = cadd(XS.ld(v, ls), dv);
-            XS.st(v, ls, xv);
-            dxn = f_max(dxn, cabsd(dv));
-            xn = f_max(xn, cabsd(xv));
-          }
-          a.sd[D_DXN * a.S + s] = dxn;
-          a.sd[D_XN * a.S + s] = xn;
-        }
-      }
-    }
-    if (mode != M_DONE && in_range)
-      for (int v = 0; v < n; ++v) X.st(v, s, XS.ld(v, ls));
-  }
-  tmem_free_cta<128>(tbase);
-}
-
-// ---------------------------------------------------------------------------------------------
 // tail mode: one warp per path slot
 // ---------------------------------------------------------------------------------------------
 // When only a few paths remain (after compaction), a thread per path leaves the GPU idle and each
@@ -1733,8 +1641,7 @@ __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
     reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, true, 4>)},                   \
    reinterpret_cast<const void*>(&pp::dev::ctrl_eval_trip<R, KM, true, (sizeof(R) < 32 ? 4 : 1)>),             \
    reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, true, 256, 2>),                                        \
-   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, false, 128, PP_LSQ_MINB, true>),                        \
-   reinterpret_cast<const void*>(&pp::dev::trips_fused<R, KM>)}
+   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, false, 128, PP_LSQ_MINB, true>)}
 
 // register-resident least-squares solvers of one level for dimension N
 #define PP_LSQ_REG(R, N)                                                                        \

@@ -37,7 +37,7 @@ CONFIGS = [
     ("katsura12_qd", "katsura12", "qd", {"max_newton": 4}, 0, 4096),
     ("rand32_d", "rand32", "d", {}, 0, 65536),
     ("rand32_dd", "rand32", "dd", {}, 0, 65536),
-    ("rand32_qd", "rand32", "qd", {}, 0, 64),
+    ("rand32_qd", "rand32", "qd", {}, 0, 4096),
 ]
 
 
@@ -123,8 +123,10 @@ def main():
                 idx = (rec["path_id"] - lo).astype(np.int64)
                 bad = 0
                 for k in KEYS:
-                    a = np.asarray(getattr(sol, k))[idx].reshape(n, -1)
-                    b = np.asarray(rec[k]).reshape(n, -1)
+                    a = np.ascontiguousarray(np.asarray(getattr(sol, k))[idx]).reshape(n, -1)
+                    b = np.ascontiguousarray(rec[k]).reshape(n, -1)
+                    if a.dtype == np.float64:  # bit patterns: -0.0 differs from 0.0
+                        a, b = a.view(np.uint64), b.view(np.uint64)
                     bad = max(bad, int(np.sum(np.any(a != b, axis=1))))
                 line["sampled_parity"] = {"paths": n, "records_differing": bad}
         print(json.dumps(line), flush=True)

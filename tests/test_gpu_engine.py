@@ -27,14 +27,14 @@ def assert_golden_ranges(sol, g, call_lo):
         assert np.array_equal(sol.path_id[off:off + per], g["path_id"][i * per:(i + 1) * per])
 
 
-@pytest.mark.parametrize("name,fused", [("cyclic10_dd_prod", None), ("cyclic10_d_prod", None),
-                                        ("cyclic10_dd_prod", "1"), ("cyclic10_dd_prod", "0")])
-def test_production_occupancy_bitwise(pp, monkeypatch, name, fused):
+@pytest.mark.parametrize("name,plain", [("cyclic10_dd_prod", False), ("cyclic10_d_prod", False),
+                                        ("cyclic10_dd_prod", True)])
+def test_production_occupancy_bitwise(pp, monkeypatch, name, plain):
     """BASELINE config 3 at the bench's size: cyclic-10 dd over 262,144 paths (592 blocks of 128
     slots, open row in TMEM, 16-trip graphs, compaction, tail mode); cyclic-10 d over 524,288 paths
     (1,024 slots per SM, register-resident solver)"""
-    if fused is not None:  # None: the default engine; "1" / "0": with and without the fused trip kernel
-        monkeypatch.setenv("PP200_FUSED", fused)
+    if plain:  # the round-1 solver: shared-memory column, no TMEM q-cache
+        monkeypatch.setenv("PP200_LSQ_QCACHE", "0")
     g = golden(f"track_{name}")
     prec = str(g["prec"])
     _, _, starts, h = homotopy(pp, read("cyclic10.sys"), prec)
@@ -81,14 +81,17 @@ def per_path(ev):
 
 
 @pytest.mark.parametrize("name", ["cyclic5_d", "cyclic5_dd", "cyclic5_d_tight"])
-@pytest.mark.parametrize("mode", ["default", "thread_per_path", "thread_per_path_fused", "warp_per_path"])
+@pytest.mark.parametrize("mode", ["default", "thread_per_path", "warp_per_path", "group8_per_path"])
 def test_step_events_match_the_reference_sink(pp, monkeypatch, name, mode):
     g = golden(f"events_{name}")
     prec = str(g["prec"])
     if mode.startswith("thread_per_path"):
         monkeypatch.setenv("PP200_TAIL_SLOTS", "0")
         monkeypatch.setenv("PP200_COOP_WHOLE_RUN", "0")
-        monkeypatch.setenv("PP200_FUSED", "1" if mode.endswith("fused") else "0")
+    elif mode == "group8_per_path":
+        monkeypatch.setenv("PP200_FORCE_COOP", "1")
+        monkeypatch.setenv("PP200_COOP_GROUP", "8")
+        monkeypatch.setenv("PP200_COOP_GROUP_EVAL", "8")
     elif mode == "warp_per_path":
         monkeypatch.setenv("PP200_FORCE_COOP", "1")
     _, _, starts, h = homotopy(pp, read("cyclic5.sys"), prec)
