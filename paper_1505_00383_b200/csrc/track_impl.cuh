@@ -574,10 +574,7 @@ struct TmemQCache {
   }
 };
 
-// kPre > 0: the first kPre rows of the next column to be projected are loaded into registers
-// before the current projection's axpy, so each dot product starts on data that arrived during
-// the axpy instead of waiting for its first global loads (needs m >= kPre).
-template <class R, class GA, class CA, bool kUniform, class QC = NoQCache, int kPre = 0>
+template <class R, class GA, class CA, bool kUniform, class QC = NoQCache>
 __device__ bool lsq_solve_c(int n, int m, double rank_tol, const GA& Q, const GA& Rm, const GA& B, const GA& Y,
                             size_t s, const CA& C, const QC& qc = QC{}) {
   // m x n (m >= n rows; the tracker's systems are square, m == n): Q column-major, element col*m + row
@@ -595,40 +592,24 @@ PP_UNROLL_ROWS
   // kUniform (warp-collective column storage): a rank-deficient lane does not leave early; it
   // finishes the solve on its own scratch with the result discarded, so the warp stays converged
   bool ok = true;
-  constexpr int P = kPre > 0 ? kPre : 1;
-  cx<R> pre[P];
-  auto load_pre = [&](int col) {
-#pragma unroll
-    for (int r = 0; r < kPre; ++r) pre[r] = Q.ld(col * m + r, s);
-  };
   for (int k = 0; k < n; ++k) {
 PP_UNROLL_ROWS
     for (int r = 0; r < m; ++r) C.st(r, Q.ld(k * m + r, s));
     const int rk = k * (k + 1) / 2;
-    if (kPre > 0 && k > 0) load_pre(0);
     for (int pass = 0; pass < 2; ++pass) {
       for (int i = 0; i < k; ++i) {
         // next column read: q_(i+1), else q_0 of the second pass, else the next column
         const int nxt = i + 1 < k ? i + 1 : (pass == 0 ? 0 : k + 1);
         if (nxt < n) prefetch_column<R>(Q, nxt, m, s);
         cx<R> rik = zero;
-#pragma unroll
-        for (int r = 0; r < kPre; ++r) {
-          qc.put(r, pre[r]);
-          rik = cadd(rik, cmul(cconj(pre[r]), C.ld(r)));
-        }
 PP_UNROLL_ROWS
-        for (int r = kPre; r < m; ++r) {
+        for (int r = 0; r < m; ++r) {
           const cx<R> q = Q.ld(i * m + r, s);
           qc.put(r, q);
           rik = cadd(rik, cmul(cconj(q), C.ld(r)));
         }
         const cx<R> prev = pass == 0 ? zero : Rm.ld(i + rk, s);
         Rm.st(i + rk, s, cadd(prev, rik));
-        if (kPre > 0) {
-          const int np = i + 1 < k ? i + 1 : (pass == 0 ? 0 : -1);  // the next projection's column
-          if (np >= 0) load_pre(np);
-        }
         qc.commit();
 PP_UNROLL_ROWS
         for (int r = 0; r < m; ++r) C.st(r, csub(C.ld(r), cmul(rik, qc.template get<R>(r, Q, i * m + r, s))));
@@ -711,7 +692,7 @@ __device__ __forceinline__ void tmem_free_cta(uint32_t base) {
 // product).  Its accesses are warp-collective, so a warp runs the solve if any lane needs it.
 // kQCache (with kTmem false): the column in shared memory, and each projected q_i cached in the
 // thread's TMEM lane between its dot product and its axpy (TmemQCache); warp-collective as well.
-template <class R, bool kTmem, int kThreads, int kMinBlocks, bool kQCache = false, int kPre = 0>
+template <class R, bool kTmem, int kThreads, int kMinBlocks, bool kQCache = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) lsq_trip(const TrackArgs a) {
   constexpr int L = level<R>::L;
   extern __shared__ double smem[];
@@ -730,8 +711,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) lsq_trip(const TrackArgs
     const TmemQCache<R> qc{base + (static_cast<uint32_t>(32 * (warp & 3)) << 16)};
     const SmemRow<R> C{Planar<R>{smem, blockDim.x}, threadIdx.x};
     if (__any_sync(0xffffffffu, need)) {
-      const bool ok = lsq_solve_c<R, decltype(J), SmemRow<R>, true, TmemQCache<R>, kPre>(n, n, a.rank_tol, J, Rm, B,
-                                                                                         Y, s, C, qc);
+      const bool ok = lsq_solve_c<R, decltype(J), SmemRow<R>, true>(n, n, a.rank_tol, J, Rm, B, Y, s, C, qc);
       if (need) si(F_OK, s) = ok ? 1 : 0;
       if (need && ok) {
         double dxn = 0.0, xn = 0.0;
@@ -1661,8 +1641,7 @@ __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
     reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, true, 4>)},                   \
    reinterpret_cast<const void*>(&pp::dev::ctrl_eval_trip<R, KM, true, (sizeof(R) < 32 ? 4 : 1)>),             \
    reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, true, 256, 2>),                                        \
-   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, false, 128, PP_LSQ_MINB, true>),                        \
-   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, false, 128, 4, true, 3>)}
+   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, false, 128, PP_LSQ_MINB, true>)}
 
 // register-resident least-squares solvers of one level for dimension N
 #define PP_LSQ_REG(R, N)                                                                        \
