@@ -324,7 +324,7 @@ void device_init(int device) {
       for (const void* k : {v[i].ctrl_eval_trip, v[i].lsq_trip, v[i].step_trip, v[i].eval, v[i].lsq, v[i].eval_coop[0],
                             v[i].eval_coop[1], v[i].eval_coop[2], v[i].lsq_coop[0], v[i].lsq_coop[1], v[i].lsq_coop[2],
                             v[i].lsq_coop_g[0], v[i].lsq_coop_g[1], v[i].lsq_coop_g[2], v[i].ctrl_eval_tmem,
-                            v[i].lsq_qcache}) {
+                            v[i].lsq_qcache, v[i].lsq_qcache_fuse}) {
         cudaFuncAttributes at;
         check(cudaFuncGetAttributes(&at, k), "kernel load");
       }
@@ -537,7 +537,8 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   // Measured on cyclic-10 dd: lsq 5.47 -> 5.33 s per 131,072 paths.
   const bool lsq_qc = !lsq_tm && !lsq_reg && tblock == 128 && env_size("PP200_LSQ_QCACHE", 1) != 0 &&
                       static_cast<size_t>(n) * 4 * L <= 128;
-  if (lsq_qc) lsq_fn = var->lsq_qcache;
+  // PP200_LSQ_FUSE=1: with the q-cache, each axpy shares its row loop with the next dot product
+  if (lsq_qc) lsq_fn = env_size("PP200_LSQ_FUSE", 0) != 0 ? var->lsq_qcache_fuse : var->lsq_qcache;
   const int lblock = lsq_tm ? 256 : tblock;
   size_t lsq_smem = (lsq_tm || lsq_reg) ? 0 : static_cast<size_t>(tblock) * per_thread_smem / 2;
   if (lsq_qc) lsq_smem = std::max<size_t>(lsq_smem, (prop.sharedMemPerMultiprocessor / 5) + 1024);

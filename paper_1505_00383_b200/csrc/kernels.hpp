@@ -129,6 +129,7 @@ struct Variant {
   const void* ctrl_eval_tmem;  // ctrl_eval_trip with the open Jacobian row in tensor memory
   const void* lsq_tmem;        // lsq_trip with the Gram-Schmidt column in tensor memory
   const void* lsq_qcache;      // lsq_trip with q_i cached in tensor memory between dot and axpy
+  const void* lsq_qcache_fuse; // the same with each axpy fused into the next dot product's row loop
 };
 
 // tail compaction: move the busy slots of [keep, n_active) into idle slots of [0, keep)

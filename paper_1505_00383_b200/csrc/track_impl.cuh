@@ -574,7 +574,12 @@ struct TmemQCache {
   }
 };
 
-template <class R, class GA, class CA, bool kUniform, class QC = NoQCache>
+// kFuse: each projection's axpy runs in the same row loop as the next projection's dot product
+// (row r of the column is updated, then multiplied into the next sum), so the independent axpy
+// rows fill the latency of the sequential sum.  Every operation and every sum order is the
+// reference's: the dot product of projection j+1 reads each row after projection j's axpy has
+// updated it, exactly as the two separate loops do.
+template <class R, class GA, class CA, bool kUniform, class QC = NoQCache, bool kFuse = false>
 __device__ bool lsq_solve_c(int n, int m, double rank_tol, const GA& Q, const GA& Rm, const GA& B, const GA& Y,
                             size_t s, const CA& C, const QC& qc = QC{}) {
   // m x n (m >= n rows; the tracker's systems are square, m == n): Q column-major, element col*m + row
@@ -596,7 +601,40 @@ PP_UNROLL_ROWS
 PP_UNROLL_ROWS
     for (int r = 0; r < m; ++r) C.st(r, Q.ld(k * m + r, s));
     const int rk = k * (k + 1) / 2;
-    for (int pass = 0; pass < 2; ++pass) {
+    if (kFuse && k > 0) {
+      // the 2k projections of column k in order: pass 0 on q_0 .. q_(k-1), then pass 1
+      cx<R> rik = zero;
+PP_UNROLL_ROWS
+      for (int r = 0; r < m; ++r) {
+        const cx<R> q = Q.ld(r, s);  // q_0
+        qc.put(r, q);
+        rik = cadd(rik, cmul(cconj(q), C.ld(r)));
+      }
+      for (int j = 0; j < 2 * k; ++j) {
+        const int pass = j >= k ? 1 : 0, i = j - pass * k;
+        const cx<R> prev = pass == 0 ? zero : Rm.ld(i + rk, s);
+        Rm.st(i + rk, s, cadd(prev, rik));
+        qc.commit();
+        if (j + 1 < 2 * k) {
+          const int in = (j + 1) % k;  // the next projection's column
+          cx<R> rnext = zero;
+PP_UNROLL_ROWS
+          for (int r = 0; r < m; ++r) {
+            const cx<R> qi = qc.template get<R>(r, Q, i * m + r, s);
+            const cx<R> c = csub(C.ld(r), cmul(rik, qi));  // axpy of projection j
+            const cx<R> qn = Q.ld(in * m + r, s);
+            qc.put(r, qn);
+            C.st(r, c);
+            rnext = cadd(rnext, cmul(cconj(qn), c));  // dot product of projection j + 1
+          }
+          rik = rnext;
+        } else {
+PP_UNROLL_ROWS
+          for (int r = 0; r < m; ++r) C.st(r, csub(C.ld(r), cmul(rik, qc.template get<R>(r, Q, i * m + r, s))));
+        }
+      }
+    }
+    for (int pass = 0; pass < 2 && !kFuse; ++pass) {
       for (int i = 0; i < k; ++i) {
         // next column read: q_(i+1), else q_0 of the second pass, else the next column
         const int nxt = i + 1 < k ? i + 1 : (pass == 0 ? 0 : k + 1);
@@ -692,7 +730,7 @@ __device__ __forceinline__ void tmem_free_cta(uint32_t base) {
 // product).  Its accesses are warp-collective, so a warp runs the solve if any lane needs it.
 // kQCache (with kTmem false): the column in shared memory, and each projected q_i cached in the
 // thread's TMEM lane between its dot product and its axpy (TmemQCache); warp-collective as well.
-template <class R, bool kTmem, int kThreads, int kMinBlocks, bool kQCache = false>
+template <class R, bool kTmem, int kThreads, int kMinBlocks, bool kQCache = false, bool kFuse = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) lsq_trip(const TrackArgs a) {
   constexpr int L = level<R>::L;
   extern __shared__ double smem[];
@@ -711,7 +749,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) lsq_trip(const TrackArgs
     const TmemQCache<R> qc{base + (static_cast<uint32_t>(32 * (warp & 3)) << 16)};
     const SmemRow<R> C{Planar<R>{smem, blockDim.x}, threadIdx.x};
     if (__any_sync(0xffffffffu, need)) {
-      const bool ok = lsq_solve_c<R, decltype(J), SmemRow<R>, true>(n, n, a.rank_tol, J, Rm, B, Y, s, C, qc);
+      const bool ok =
+          lsq_solve_c<R, decltype(J), SmemRow<R>, true, TmemQCache<R>, kFuse>(n, n, a.rank_tol, J, Rm, B, Y, s, C, qc);
       if (need) si(F_OK, s) = ok ? 1 : 0;
       if (need && ok) {
         double dxn = 0.0, xn = 0.0;
@@ -1641,7 +1680,8 @@ __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
     reinterpret_cast<const void*>(&pp::dev::lsq_coop<R, true, 4>)},                   \
    reinterpret_cast<const void*>(&pp::dev::ctrl_eval_trip<R, KM, true, (sizeof(R) < 32 ? 4 : 1)>),             \
    reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, true, 256, 2>),                                        \
-   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, false, 128, PP_LSQ_MINB, true>)}
+   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, false, 128, PP_LSQ_MINB, true>),                        \
+   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, false, 128, PP_LSQ_MINB, true, true>)}
 
 // register-resident least-squares solvers of one level for dimension N
 #define PP_LSQ_REG(R, N)                                                                        \
