@@ -55,3 +55,33 @@ def test_acceptance_criteria_4_and_6_on_the_device():
     assert r.returncode == 0, r.stdout + r.stderr[-2000:]
     assert "[PASS] gpu criterion  4" in r.stdout and "[PASS] gpu criterion  6" in r.stdout
     assert r.stdout.count("bitwise equal to the reference: yes") == 2
+
+
+@pytest.mark.parametrize("name,prec,cfg", [("cyclic5_d", "d", []), ("cyclic5_dd", "dd", []),
+                                          ("cyclic5_d_tight", "d", ["2", "0.1", "40"])])
+def test_progress_sink_through_the_shim(name, prec, cfg):
+    """a reference-API caller passes a ProgressSink to polypath::track_all<R>; through the shim the
+    device's events reach it, and per path they equal the reference sink's (field for field)"""
+    import numpy as np
+
+    from conftest import golden
+
+    exe = os.path.join(ROOT, "oracle", "_ref", "shim_events")
+    if not os.path.exists(exe):
+        pytest.fail("oracle/_ref/shim_events is not built (oracle/Makefile target `acceptance`)")
+    r = subprocess.run([exe, os.path.join(ROOT, "tests", "data", "cyclic5.sys"), prec, *cfg], capture_output=True,
+                       text=True, timeout=600, env=dict(os.environ, POLYPATH_B200_TRACE="1"))
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "[pp200] track_all" in r.stderr
+    rows = [ln.split() for ln in r.stdout.splitlines()]
+    got = [(int(a), int(b, 16), int(c, 16), int(d), int(e), int(f)) for a, b, c, d, e, f in rows]
+    want = golden(f"events_{name}")["events"]
+    assert len(got) == len(want)
+    order_g = sorted(range(len(got)), key=lambda i: (got[i][0], i))
+    order_w = np.argsort(want["path_id"], kind="stable")
+    for ig, iw in zip(order_g, order_w):
+        w = want[iw]
+        assert got[ig][0] == int(w["path_id"])
+        assert got[ig][1] == int(np.float64(w["t"]).view(np.uint64))
+        assert got[ig][2] == int(np.float64(w["h"]).view(np.uint64))
+        assert (got[ig][3], got[ig][4], got[ig][5]) == (int(w["newton_iters"]), int(w["status"]), int(w["accepted"]))
