@@ -689,6 +689,8 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   float kms[3] = {0, 0, 0};  // eval (thread mode: control + evaluation), lsq, tail-mode control
   a.n_active = S;
   a.tmem_cols = tmem_cols;
+  // PP200_LSQ_SPT: slots per thread of the q-cache solver (1 or 2)
+  a.lsq_spt = lsq_qc ? static_cast<int>(std::min<size_t>(2, std::max<size_t>(1, env_size("PP200_LSQ_SPT", 1)))) : 1;
   {
     const dim3 blk(tblock);
     dim3 grid(static_cast<unsigned>(blocks));
@@ -780,8 +782,9 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
         check(cudaLaunchKernel(ctrl_eval_fn, egrid(), dim3(eblock), args, eval_smem, stream),
               "launch ctrl_eval_trip");
         if (ev) check(cudaEventRecord(ev[2], stream), "event");
-        check(cudaLaunchKernel(lsq_fn, dim3(static_cast<unsigned>((a.n_active + lblock - 1) / lblock)), dim3(lblock), targs,
-                               lsq_smem, stream),
+        const size_t per_block = static_cast<size_t>(lblock) * a.lsq_spt;
+        check(cudaLaunchKernel(lsq_fn, dim3(static_cast<unsigned>((a.n_active + per_block - 1) / per_block)), dim3(lblock),
+                               targs, lsq_smem, stream),
               "launch lsq_trip");
       }
       if (ev) check(cudaEventRecord(ev[3], stream), "event");

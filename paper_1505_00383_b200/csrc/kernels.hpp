@@ -67,6 +67,7 @@ struct TrackArgs {
   unsigned long long* work;  // [0] evaluations, [1] least-squares solves issued
   // per-slot storage (S slots).  Planar arrays: element e, limb-plane p, slot s at ((e*P)+p)*S+s.
   uint32_t tmem_cols;  // tensor-memory columns per CTA of ctrl_eval_trip<..., kTmem = true>
+  int lsq_spt;         // slots per thread of the q-cache solver (its grid covers n_active / lsq_spt)
   size_t S;         // slot stride of the planar arrays
   size_t n_active;  // slots [0, n_active) are launched (shrinks when the tail is compacted)
   int32_t* si;                  // integer state, field f at f*S + s (track_impl.cuh F_*)

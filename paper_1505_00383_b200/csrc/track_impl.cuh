@@ -748,21 +748,30 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) lsq_trip(const TrackArgs
     const int warp = threadIdx.x >> 5;
     const TmemQCache<R> qc{base + (static_cast<uint32_t>(32 * (warp & 3)) << 16)};
     const SmemRow<R> C{Planar<R>{smem, blockDim.x}, threadIdx.x};
-    if (__any_sync(0xffffffffu, need)) {
+    // a.lsq_spt slots per thread, one after the other (slot s, s + grid, ...): fewer slots in
+    // flight keep more of their Q columns resident in L2 between projections
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (int rep = 0; rep < a.lsq_spt; ++rep) {
+      const size_t sr = s + rep * stride;
+      const bool in_r = sr < a.n_active;
+      const int mode_r = in_r ? si(F_MODE, sr) : M_DONE;
+      const bool need_r = mode_r == M_NEWTON || mode_r == M_REFINE;
+      if (!__any_sync(0xffffffffu, need_r)) continue;
+      const size_t so = in_r ? sr : s;  // out-of-range lanes run on their first slot's scratch
       const bool ok =
-          lsq_solve_c<R, decltype(J), SmemRow<R>, true, TmemQCache<R>, kFuse>(n, n, a.rank_tol, J, Rm, B, Y, s, C, qc);
-      if (need) si(F_OK, s) = ok ? 1 : 0;
-      if (need && ok) {
+          lsq_solve_c<R, decltype(J), SmemRow<R>, true, TmemQCache<R>, kFuse>(n, n, a.rank_tol, J, Rm, B, Y, so, C, qc);
+      if (need_r) si(F_OK, sr) = ok ? 1 : 0;
+      if (need_r && ok) {
         double dxn = 0.0, xn = 0.0;
         for (int v = 0; v < n; ++v) {
           const cx<R> dv = C.ld(v);
-          const cx<R> xv = cadd(X.ld(v, s), dv);
-          X.st(v, s, xv);
+          const cx<R> xv = cadd(X.ld(v, sr), dv);
+          X.st(v, sr, xv);
           dxn = f_max(dxn, cabsd(dv));
           xn = f_max(xn, cabsd(xv));
         }
-        a.sd[D_DXN * a.S + s] = dxn;
-        a.sd[D_XN * a.S + s] = xn;
+        a.sd[D_DXN * a.S + sr] = dxn;
+        a.sd[D_XN * a.S + sr] = xn;
       }
     }
     tmem_free_cta<128>(base);
