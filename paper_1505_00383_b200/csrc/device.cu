@@ -535,10 +535,13 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   // TMEM between its dot product and its axpy (128 columns per CTA; the shared memory request is
   // padded so that at most four CTAs are resident per SM and every tcgen05.alloc succeeds at once).
   // Measured on cyclic-10 dd: lsq 5.47 -> 5.33 s per 131,072 paths.
-  const bool lsq_qc = !lsq_tm && !lsq_reg && tblock == 128 && env_size("PP200_LSQ_QCACHE", 1) != 0 &&
+  // Double-double only: in complex double the cache costs more than the re-read it saves
+  // (rand32 d: 3,610 -> 3,102 paths/s).
+  const bool lsq_qc = !lsq_tm && !lsq_reg && tblock == 128 && env_size("PP200_LSQ_QCACHE", L == 2 ? 1 : 0) != 0 &&
                       static_cast<size_t>(n) * 4 * L <= 128;
-  // PP200_LSQ_FUSE=1: with the q-cache, each axpy shares its row loop with the next dot product
-  if (lsq_qc) lsq_fn = env_size("PP200_LSQ_FUSE", 0) != 0 ? var->lsq_qcache_fuse : var->lsq_qcache;
+  // PP200_LSQ_FUSE (default 1): with the q-cache, each axpy shares its row loop with the next dot
+  // product (cyclic-10 dd: lsq 9.73 -> 9.54 s per 262,144 paths; cyclic-8 dd +2.3 %)
+  if (lsq_qc) lsq_fn = env_size("PP200_LSQ_FUSE", 1) != 0 ? var->lsq_qcache_fuse : var->lsq_qcache;
   const int lblock = lsq_tm ? 256 : tblock;
   size_t lsq_smem = (lsq_tm || lsq_reg) ? 0 : static_cast<size_t>(tblock) * per_thread_smem / 2;
   if (lsq_qc) lsq_smem = std::max<size_t>(lsq_smem, (prop.sharedMemPerMultiprocessor / 5) + 1024);
@@ -747,11 +750,12 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     // PP200_FORCE_COOP=1 runs every trip in tail mode (used by the parity tests)
     // small runs (no more paths than tail slots) start in tail mode: a warp per path spreads a
     // few thousand paths over every SM instead of packing them into a few blocks
-    // Whole runs also stay in tail mode where a thread per path cannot fill the SMs: quad-double
-    // (its per-thread working set leaves a few warps per SM; katsura-12 qd: 80.5 s thread per path
-    // against 21.6 s with groups of 8 lanes) and any system whose point and open Jacobian row
-    // shrink the trip blocks below 128 threads (rand32 dd, n = 32: 148 -> 184 paths/s).
-    const bool coop_whole_run = env_size("PP200_COOP_WHOLE_RUN", 1) != 0 && (plan.prec == 2 || tblock < 128);
+    // Whole quad-double runs stay in tail mode: a thread per path leaves a few warps per SM for
+    // its per-thread working set (katsura-12 qd: 80.5 s thread per path against 21.6 s with
+    // groups of 8 lanes).  Large double-double systems do not: rand32 dd over all 65,536 paths
+    // runs at 408 paths/s a thread per path against 290 in tail mode (a 8,192-path sample
+    // favoured tail mode, 184 vs 148: its tail dominates).
+    const bool coop_whole_run = env_size("PP200_COOP_WHOLE_RUN", 1) != 0 && plan.prec == 2;
     bool coop = (env_size("PP200_FORCE_COOP", 0) != 0 || coop_whole_run || (tail_slots > 0 && count <= tail_slots)) &&
                 coop_ok;
     // one trip = control (step control, prediction, finalize, refill) followed by the heavy
