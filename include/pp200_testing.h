@@ -32,6 +32,13 @@ int pp_fp64_peak(int device, double* ops_per_s);
 /* n doubles formatted as the JSON-lines records print them (nlohmann::json 3.11's dump()),
  * newline-separated; *needed = bytes including the NUL (PP_E_CAPACITY when cap is too small) */
 int pp_test_json_doubles(const double* v, size_t n, char* buf, size_t cap, size_t* needed);
+/* The corrector alone, as the reference's tests drive it through PathBatch::set_prediction and
+ * newton_correct (tracker.hpp:135-136, tracker.cpp:216-274): for each of `batch` pairs (t [L], x
+ * [dim][2L]) run up to cfg->max_newton Newton iterations at that t on the device.  Outputs the
+ * iterations performed (last_iterations), whether the residual / update test certified the step
+ * (last_corrected), whether a solve was rank-deficient, and the last iterate (in place in x). */
+int pp_test_newton(const pp_homotopy* h, const pp_track_config* cfg, uint32_t batch, const double* t, double* x,
+                   uint32_t* iters, uint8_t* corrected, uint8_t* singular, int device);
 /* [mon_steps, cmul_steps, jac_terms, jac_scaled, n_base] of a homotopy's plan */
 int pp_homotopy_counts(const pp_homotopy* h, uint64_t* counts);
 

@@ -86,6 +86,8 @@ if ref is not None:
     ref.ref_track_events.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, _i32, _vp,
                                      ctypes.POINTER(TrackConfigC), _u64, _u64, ctypes.POINTER(RecordsC), _vp, _u64,
                                      ctypes.POINTER(_u64)]
+    ref.ref_newton.argtypes = [ctypes.c_char_p, ctypes.c_char_p, _i32, _vp, ctypes.POINTER(TrackConfigC), _u32, _vp, _vp,
+                               _vp, _vp, ctypes.POINTER(_u32)]
     ref.ref_eval.argtypes = [ctypes.c_char_p, ctypes.c_char_p, _i32, _vp, _u32, _vp, _vp, _vp, _vp]
     ref.ref_lsq.argtypes = [_i32, _u32, _u32, _vp, _vp, _vp, _vp]
     ref.ref_td_solution.argtypes = [ctypes.c_char_p, _i32, _u64, _vp]
@@ -196,6 +198,27 @@ def ref_track_events(f_text: str, prec: str, gamma: complex, cfg: dict | None = 
         raise RuntimeError("event capacity exceeded")
     k = rec.count
     return {key: v[:k].copy() for key, v in arrs.items()}, ev[:n_ev.value].copy()
+
+
+def ref_newton(f_text: str, prec: str, gamma_limbs: np.ndarray, t: np.ndarray, x: np.ndarray, cfg: dict | None = None,
+               g_text: str | None = None):
+    """PathBatch::set_prediction + newton_correct of the reference (tracker.hpp:135-136) for the
+    pairs t [B][L], x [B][dim][2L]; returns (iterations, corrected, last iterates, rounds)"""
+    _need(ref, "reference build")
+    c = TrackConfigC()
+    ref.ref_track_config_defaults(PREC[prec], ctypes.byref(c))
+    for k, v in (cfg or {}).items():
+        setattr(c, k, v)
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    xo = np.ascontiguousarray(x, dtype=np.float64).copy()
+    B = len(t)
+    it = np.zeros(B, np.uint32)
+    co = np.zeros(B, np.uint8)
+    rounds = _u32()
+    gl = np.ascontiguousarray(gamma_limbs, dtype=np.float64)
+    _chk(ref.ref_newton(f_text.encode(), g_text.encode() if g_text else None, PREC[prec], _ptr(gl), ctypes.byref(c), B,
+                        _ptr(t), _ptr(xo), _ptr(it), _ptr(co), ctypes.byref(rounds)))
+    return it, co.astype(bool), xo, rounds.value
 
 
 def ref_eval(f_text: str, prec: str, gamma_limbs: np.ndarray, points: np.ndarray, t: np.ndarray,

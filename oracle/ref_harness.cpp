@@ -313,7 +313,48 @@ int dispatch(int prec, F&& f) {
 
 }  // namespace
 
+// PathBatch::set_prediction + newton_correct (tracker.hpp:135-136, tracker.cpp:216-274) for
+// `batch` (t, x) pairs on f with start g and gamma (2L limbs), cohort width = batch
+template <class R>
+int newton_impl(const char* f_text, const char* g_text, const double* gamma, const pp_track_config* c, uint32_t batch,
+                const double* t, double* x, uint32_t* iters, uint8_t* corrected, uint32_t* rounds) {
+  PolySystem f = parse_system(f_text);
+  PolySystem g = g_text ? parse_system(g_text) : total_degree_start<R>(f).first;
+  auto h = make_homotopy<R>(f, g, Cplx<R>{get_real<R>(gamma), get_real<R>(gamma + limbs_of<R>())});
+  TrackConfig cfg = to_cfg(c);
+  const uint32_t dim = f.dim;
+  const int L = limbs_of<R>();
+  PathBatch<R> b(h, cfg, batch);
+  std::vector<Cplx<R>> xs(dim);
+  for (uint32_t i = 0; i < batch; ++i) {
+    for (uint32_t v = 0; v < dim; ++v) xs[v] = get_cplx<R>(x + (static_cast<size_t>(i) * dim + v) * 2 * L);
+    b.seed(i, xs);
+  }
+  for (uint32_t i = 0; i < batch; ++i) {
+    for (uint32_t v = 0; v < dim; ++v) xs[v] = get_cplx<R>(x + (static_cast<size_t>(i) * dim + v) * 2 * L);
+    b.set_prediction(i, get_real<R>(t + static_cast<size_t>(i) * L), xs);
+  }
+  *rounds = b.newton_correct();
+  for (uint32_t i = 0; i < batch; ++i) {
+    iters[i] = b.last_iterations(i);
+    corrected[i] = b.last_corrected(i) ? 1 : 0;
+    auto w = b.working_point(i);
+    for (uint32_t v = 0; v < dim; ++v) put_cplx(w[v], x + (static_cast<size_t>(i) * dim + v) * 2 * L);
+  }
+  return PP_OK;
+}
+
 extern "C" {
+
+int ref_newton(const char* f_text, const char* g_text, int prec, const double* gamma, const pp_track_config* cfg,
+               uint32_t batch, const double* t, double* x, uint32_t* iters, uint8_t* corrected, uint32_t* rounds) {
+  return guarded([&] {
+    return dispatch(prec, [&](auto tag) {
+      using R = decltype(tag);
+      return newton_impl<R>(f_text, g_text, gamma, cfg, batch, t, x, iters, corrected, rounds);
+    });
+  });
+}
 
 const char* ref_last_error(void) { return g_err.c_str(); }
 

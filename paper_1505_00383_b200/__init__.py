@@ -161,6 +161,7 @@ _sig("pp_system_from_terms", _i32, _u32, _u32, _vp, _vp, _vp, _vp, _P(_vp))
 _sig("pp_device_count", _i32)
 _sig("pp_device_init", _i32, _i32)
 _sig("pp_test_json_doubles", _i32, _vp, _sz, ctypes.c_char_p, _sz, _P(_sz))
+_sig("pp_test_newton", _i32, _vp, _P(TrackConfigC), _u32, _vp, _vp, _vp, _vp, _vp, _i32)
 _sig("pp_system_print", _i32, _vp, ctypes.c_char_p, _sz, _P(_sz))
 _sig("pp_system_stats", _i32, _vp, _P(_u32), _P(_u32), _P(_u64), _P(_u64), _P(_i32))
 _sig("pp_system_degrees", _i32, _vp, _vp)
@@ -677,6 +678,23 @@ def lsq_batch_mn(prec, a: np.ndarray, b: np.ndarray, device: int = 0, factors: b
     _check(lib.pp_lsq_batch_mn(_prec(prec), m, n, B, _ptr(a), _ptr(b), _ptr(x), _ptr(ok),
                                _ptr(q) if factors else None, _ptr(r) if factors else None, device))
     return (x, ok.astype(bool), q, r) if factors else (x, ok.astype(bool))
+
+
+def newton_correct(h: Homotopy, t: np.ndarray, x: np.ndarray, cfg: TrackConfig | None = None, device: int = 0):
+    """The corrector alone, as PathBatch::set_prediction + newton_correct drive it
+    (tracker.hpp:135-136, tracker.cpp:216-274): for each pair (t [B][L], x [B][dim][2L]) up to
+    max_newton Newton iterations at that t on the device.  Returns (iterations, corrected,
+    singular, last iterates)."""
+    cfg = cfg or TrackConfig.defaults(h.prec)
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    xo = np.ascontiguousarray(x, dtype=np.float64).copy()
+    B = len(t)
+    it = np.zeros(B, np.uint32)
+    co = np.zeros(B, np.uint8)
+    sg = np.zeros(B, np.uint8)
+    c = cfg.to_c()
+    _check(lib.pp_test_newton(h._h, ctypes.byref(c), B, _ptr(t), _ptr(xo), _ptr(it), _ptr(co), _ptr(sg), device))
+    return it, co.astype(bool), sg.astype(bool), xo
 
 
 def fp64_peak(device: int = 0) -> float:

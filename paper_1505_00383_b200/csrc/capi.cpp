@@ -795,4 +795,17 @@ int pp_test_json_doubles(const double* v, size_t n, char* buf, size_t cap, size_
   return PP_OK;
 }
 
+// PathBatch::set_prediction + newton_correct (tracker.hpp:135-136, tracker.cpp:216-274) on the device
+int pp_test_newton(const pp_homotopy* h, const pp_track_config* cfg, uint32_t batch, const double* t, double* x,
+                   uint32_t* iters, uint8_t* corrected, uint8_t* singular, int device) {
+  int rc = pp_track_config_validate(cfg);
+  if (rc != PP_OK) return rc;
+  return guard([&] {
+    need(h != nullptr && (batch == 0 || (t && x && iters && corrected && singular)), "pp_test_newton: null argument");
+    pp_homotopy* hm = const_cast<pp_homotopy*>(h);
+    pp::device_newton(hm->plan, hm->on(device), *cfg, batch, t, x, iters, corrected, singular, device);
+    return PP_OK;
+  });
+}
+
 }  // extern "C"

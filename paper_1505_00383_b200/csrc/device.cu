@@ -1071,6 +1071,53 @@ double device_bench_eval(const Plan& plan, DevicePlan* dp, uint32_t batch, const
   return ms / std::max<uint32_t>(reps, 1);
 }
 
+// the corrector alone for `batch` (t, x) pairs (layouts of pp_test_newton)
+void device_newton(const Plan& plan, DevicePlan* dp, const pp_track_config& cfg, uint32_t batch, const double* t,
+                   double* x, uint32_t* iters, uint8_t* corrected, uint8_t* singular, int device) {
+  if (batch == 0) return;
+  DeviceGuard g(device);
+  const uint32_t n = plan.dim, L = plan.L, w = 2 * L;
+  const dev::Variant* var = pick_variant(plan.prec, n, plan.max_k);
+  if (var == nullptr) throw InvalidArgument("system beyond the compiled kernels");
+  check_planar_size(static_cast<size_t>(n) * n * w * batch, "pp_test_newton");
+  std::vector<double> xp(static_cast<size_t>(batch) * n * w), tp(static_cast<size_t>(batch) * L);
+  to_planar(x, xp.data(), batch, n, w);
+  to_planar(t, tp.data(), batch, 1, L);
+  DevBuf<double> dx(xp), dt(tp), dj(static_cast<size_t>(batch) * n * n * w),
+      dr(static_cast<size_t>(batch) * n * (n + 1) / 2 * w), db(static_cast<size_t>(batch) * n * w),
+      dy(static_cast<size_t>(batch) * n * w);
+  DevBuf<uint32_t> di(batch);
+  DevBuf<uint8_t> dc(batch), ds(batch);
+  dev::NewtonArgs a{};
+  a.plan = plan_args(plan, dp);
+  a.batch = batch;
+  a.max_newton = cfg.max_newton;
+  a.rtol = cfg.residual_tol;
+  a.utol = cfg.update_tol;
+  a.rank_tol = default_rank_tol(plan.prec);
+  a.x = dx.p;
+  a.t = dt.p;
+  a.J = dj.p;
+  a.Rm = dr.p;
+  a.B = db.p;
+  a.Y = dy.p;
+  a.iters = di.p;
+  a.corrected = dc.p;
+  a.singular = ds.p;
+  int block = 128;
+  while (block > 32 && static_cast<size_t>(block) * 3 * n * w * sizeof(double) > 200 * 1024) block /= 2;
+  const size_t smem = static_cast<size_t>(block) * 3 * n * w * sizeof(double);
+  ensure_smem(var->newton, smem, device);
+  void* args[] = {&a};
+  check(cudaLaunchKernel(var->newton, dim3((batch + block - 1) / block), dim3(block), args, smem, 0), "launch newton");
+  check(cudaDeviceSynchronize(), "newton kernel");
+  check(cudaMemcpy(xp.data(), dx.p, xp.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+  check(cudaMemcpy(iters, di.p, batch * 4, cudaMemcpyDeviceToHost), "D2H");
+  check(cudaMemcpy(corrected, dc.p, batch, cudaMemcpyDeviceToHost), "D2H");
+  check(cudaMemcpy(singular, ds.p, batch, cudaMemcpyDeviceToHost), "D2H");
+  from_planar(xp.data(), x, batch, n, w);
+}
+
 void device_lsq(int prec, uint32_t m, uint32_t n, uint32_t batch, const double* a, const double* b, double* x,
                 uint8_t* ok, double* q_out, double* r_out, int device) {
   if (batch == 0) return;

@@ -47,6 +47,10 @@ double device_bench_eval(const Plan& plan, DevicePlan* dp, uint32_t batch, const
 void device_lsq(int prec, uint32_t m, uint32_t n, uint32_t batch, const double* a, const double* b, double* x,
                 uint8_t* ok, double* q_out, double* r_out, int device);
 
+// the corrector alone for `batch` (t, x) pairs (pp_test_newton)
+void device_newton(const Plan& plan, DevicePlan* dp, const pp_track_config& cfg, uint32_t batch, const double* t,
+                   double* x, uint32_t* iters, uint8_t* corrected, uint8_t* singular, int device);
+
 // rank tolerance of the reference's least_squares_solve default (linalg.hpp:44-52)
 inline double default_rank_tol(int prec) { return prec == 0 ? 1e-8 : (prec == 1 ? 1e-16 : 1e-32); }
 

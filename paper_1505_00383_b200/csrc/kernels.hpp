@@ -116,6 +116,20 @@ struct LsqArgs {
 
 constexpr int kCoopGroups[3] = {32, 8, 4};
 
+// the corrector alone for independent (t, x) pairs (one thread per pair)
+struct NewtonArgs {
+  PlanArgs plan;
+  uint32_t batch;
+  int max_newton;
+  double rtol, utol, rank_tol;
+  double* x;        // planar, S = batch: element v (in: prediction, out: last iterate)
+  const double* t;  // planar real, element 0
+  double *J, *Rm, *B, *Y;  // planar scratch
+  uint32_t* iters;
+  uint8_t* corrected;
+  uint8_t* singular;
+};
+
 struct Variant {
   int kmax;
   const void* ctrl_eval_trip;  // __global__ void(TrackArgs, unsigned* busy): control + evaluation
@@ -131,6 +145,7 @@ struct Variant {
   const void* lsq_tmem;        // lsq_trip with the Gram-Schmidt column in tensor memory
   const void* lsq_qcache;      // lsq_trip with q_i cached in tensor memory between dot and axpy
   const void* lsq_qcache_fuse; // the same with each axpy fused into the next dot product's row loop
+  const void* newton;          // __global__ void(NewtonArgs): the corrector alone (set_prediction tests)
 };
 
 // tail compaction: move the busy slots of [keep, n_active) into idle slots of [0, keep)

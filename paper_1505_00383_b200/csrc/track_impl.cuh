@@ -1655,6 +1655,56 @@ __global__ void __launch_bounds__(128) eval_kernel(const EvalArgs a) {
   for (int p = 0; p < a.plan.n_polys; ++p) B.st(p, s, cneg(B.ld(p, s)));
 }
 
+// The corrector alone (PathBatch::newton_correct after set_prediction, tracker.cpp:216-274 and
+// tracker.hpp:135-136): each thread runs up to max_newton Newton iterations at its own (t, x):
+// evaluation, least squares, x += dx, the residual / update test -- the same operations the
+// tracker's corrector performs -- and reports the iterations, the convergence and singularity
+// flags and the final iterate.  Shared memory per thread: the point, the open Jacobian row and the
+// Gram-Schmidt column.
+template <class R, int KMAX>
+__global__ void __launch_bounds__(128) newton_kernel(const NewtonArgs a) {
+  constexpr int L = level<R>::L;
+  extern __shared__ double smem[];
+  const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= a.batch) return;
+  const int n = a.plan.n;
+  const size_t ls = threadIdx.x, col = static_cast<size_t>(n) * 2 * L * blockDim.x;
+  const Planar<R> XS{smem, blockDim.x}, JR{smem + col, blockDim.x};
+  const SmemRow<R> C{Planar<R>{smem + 2 * col, blockDim.x}, ls};
+  const Planar<R> XG{a.x, a.batch}, TG{const_cast<double*>(a.t), a.batch};
+  const Planar<R> J{a.J, a.batch}, Rm{a.Rm, a.batch}, B{a.B, a.batch}, Y{a.Y, a.batch};
+  for (int v = 0; v < n; ++v) XS.st(v, ls, XG.ld(v, s));
+  const R t = TG.ldr(0, s);
+  uint32_t iters = 0;
+  uint8_t corrected = 0, sing = 0;
+  for (int it = 0; it < a.max_newton; ++it) {
+    ++iters;
+    double resid;
+    R resid_r;
+    eval_hj<R, KMAX>(a.plan, XS, SmemRow<R>{JR, ls}, ls, t, B, J, s, resid, resid_r);
+    if (!lsq_solve_c<R, Planar<R>, SmemRow<R>, false>(n, n, a.rank_tol, J, Rm, B, Y, s, C)) {
+      sing = 1;
+      break;
+    }
+    double dxn = 0.0, xn = 0.0;
+    for (int v = 0; v < n; ++v) {
+      const cx<R> dv = C.ld(v);
+      const cx<R> xv = cadd(XS.ld(v, ls), dv);
+      XS.st(v, ls, xv);
+      dxn = f_max(dxn, cabsd(dv));
+      xn = f_max(xn, cabsd(xv));
+    }
+    if (resid <= a.rtol && dxn <= f_mul(a.utol, f_max(1.0, xn))) {
+      corrected = 1;
+      break;
+    }
+  }
+  for (int v = 0; v < n; ++v) XG.st(v, s, XS.ld(v, ls));
+  a.iters[s] = iters;
+  a.corrected[s] = corrected;
+  a.singular[s] = sing;
+}
+
 template <class R>
 __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
   extern __shared__ double smem[];
@@ -1690,7 +1740,8 @@ __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
    reinterpret_cast<const void*>(&pp::dev::ctrl_eval_trip<R, KM, true, (sizeof(R) < 32 ? 4 : 1)>),             \
    reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, true, 256, 2>),                                        \
    reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, false, 128, PP_LSQ_MINB, true>),                        \
-   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, false, 128, PP_LSQ_MINB, true, true>)}
+   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, false, 128, PP_LSQ_MINB, true, true>),                  \
+   reinterpret_cast<const void*>(&pp::dev::newton_kernel<R, KM>)}
 
 // register-resident least-squares solvers of one level for dimension N
 #define PP_LSQ_REG(R, N)                                                                        \

@@ -153,3 +153,40 @@ def test_two_ranks_share_the_gpu(tmp_path):
         assert np.array_equal(z["path_id"], np.arange(0, 512, dtype=np.uint64))
         for k in TRACK_KEYS:
             assert np.array_equal(bits(z[k]), bits(g[k])), k
+
+
+def newton_cases():
+    import os
+
+    from conftest import GOLDEN
+
+    z = np.load(os.path.join(GOLDEN, "newton_cases.npz"))
+    return [str(n) for n in z["names"]], z
+
+
+@pytest.mark.parametrize("name", newton_cases()[0])
+def test_corrector_alone_matches_set_prediction(pp, name):
+    """PathBatch::set_prediction + newton_correct (tracker.hpp:135-136; test_tracker.cpp:121-196,
+    acceptance criterion 9): on-path, nearby, hopeless and rank-deficient predictions give the
+    reference's iteration counts, certification flags and last iterates, bit for bit; the square
+    homotopy reproduces the reference tests' expectations (one iteration on the path, 2.1 -> 2 in
+    three, the lockstep pattern (3, 1, 2), no convergence from (250, 40) with max_newton = 2)"""
+    _, z = newton_cases()
+    g = {k.split("__", 1)[1]: z[k] for k in z.files if k.startswith(name + "__")}
+    prec = str(g["prec"])
+    L = pp.LIMBS[prec]
+    f = pp.parse_system(str(g["f"]))
+    gs = pp.parse_system(str(g["g"])) if str(g["g"]) else pp.total_degree_start(f, prec)[0]
+    gam = complex(g["gamma"][0], g["gamma"][L])
+    h = pp.make_homotopy(f, gs, gam, prec)
+    cfg = pp.TrackConfig.defaults(prec)
+    for k, v in eval(str(g["cfg"])).items():
+        setattr(cfg, k, v)
+    it, co, sg, xo = pp.newton_correct(h, g["t"], g["x"], cfg)
+    assert np.array_equal(it, g["iters"])
+    assert np.array_equal(co, g["corrected"])
+    assert np.array_equal(bits(xo), bits(g["x_out"]))
+    if name == "square_d":
+        assert it.tolist()[:2] == [1, 3] and it.tolist()[4:] == [3, 1, 2] and co[0] and co[2]
+    if name.startswith("cyclic"):
+        assert sg[-1] and it[-1] == 1  # the origin: rank-deficient Jacobian, the solve fails at once
