@@ -4,7 +4,7 @@ double-double on 1..8 B200 (BASELINE.json metric), against the reference CPU tra
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--paths B]
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
 
-A step tracks B start paths per GPU of the 3,628,800-path total-degree start set to their terminal
+A step tracks B (default 393,216) start paths per GPU of the 3,628,800-path total-degree start set to their terminal
 status (success / failed / diverged after finalize).  Step s takes a contiguous chunk of N*B start
 indices, spread over the index space by a golden-ratio sequence, and rank r tracks the block-cyclic
 shard r of it (blocks of 64 indices, pp_shard), so N GPUs do N times the work (weak scaling) with
@@ -437,7 +437,11 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--paths", type=int, default=262144, help="start paths per step per GPU")
+    # 393,216 paths per step and GPU: the per-step tail (the last, longest paths of a call running
+    # on few SMs) costs less than at 262,144 (17.9 k against 17.5 k paths/s measured), while a
+    # 25-step driver run still takes about ten minutes; the whole 3,628,800-path job in one call
+    # runs at 18.6 k (profiles/r02/full_cyclic10_dd.json)
+    ap.add_argument("--paths", type=int, default=393216, help="start paths per step per GPU (multiple of 64)")
     ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of reference CPU tracking per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--launch-check", action="store_true",
