@@ -66,9 +66,11 @@ struct DevBuf {
   }
 };
 
+// the allocation is padded to a multiple of 16 bytes (bulk copies move whole 16-byte units)
 template <class T>
 T* upload(const std::vector<T>& v) {
-  T* p = dmalloc<T>(v.size());
+  const size_t bytes = (v.size() * sizeof(T) + 15) / 16 * 16;
+  T* p = dmalloc<T>((bytes + sizeof(T) - 1) / sizeof(T));
   if (!v.empty()) check(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
   return p;
 }
@@ -324,7 +326,7 @@ void device_init(int device) {
       for (const void* k : {v[i].ctrl_eval_trip, v[i].lsq_trip, v[i].step_trip, v[i].eval, v[i].lsq, v[i].eval_coop[0],
                             v[i].eval_coop[1], v[i].eval_coop[2], v[i].lsq_coop[0], v[i].lsq_coop[1], v[i].lsq_coop[2],
                             v[i].lsq_coop_g[0], v[i].lsq_coop_g[1], v[i].lsq_coop_g[2], v[i].ctrl_eval_tmem,
-                            v[i].lsq_qcache, v[i].lsq_qcache_fuse}) {
+                            v[i].lsq_qcache, v[i].lsq_qcache_fuse, v[i].ctrl_eval_tmem_staged}) {
         cudaFuncAttributes at;
         check(cudaFuncGetAttributes(&at, k), "kernel load");
       }
@@ -513,7 +515,24 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
                tmem_cols <= 512;
   }
   const void* ctrl_eval_fn = tmem ? var->ctrl_eval_tmem : var->ctrl_eval_trip;
-  const size_t eval_smem = static_cast<size_t>(eblock) * per_thread_smem / (tmem ? 2 : 1);
+  size_t eval_smem = static_cast<size_t>(eblock) * per_thread_smem / (tmem ? 2 : 1);
+  // PP200_STAGE_TABLES=1 (TMEM evaluation): the plan tables go to shared memory by bulk TMA copies
+  // when each CTA starts, and the evaluation reads them from there
+  dev::PlanArgs staged_plan = plan_args(plan, dp);
+  if (tmem && env_size("PP200_STAGE_TABLES", 0) != 0) {
+    auto r16 = [](size_t b) { return static_cast<uint32_t>((b + 15) / 16 * 16); };
+    staged_plan.stage_bytes[0] = r16(plan.term_info.size() * sizeof(int32_t));
+    staged_plan.stage_bytes[1] = r16(plan.pos.size() * sizeof(uint32_t));
+    staged_plan.stage_bytes[2] = r16(plan.base.size() * sizeof(uint32_t));
+    staged_plan.stage_bytes[3] = r16(plan.coeff.size() * sizeof(double));
+    staged_plan.stage_bytes[4] =
+        staged_plan.stage_bytes[0] + staged_plan.stage_bytes[1] + staged_plan.stage_bytes[2] + staged_plan.stage_bytes[3];
+    staged_plan.stage_offset = static_cast<uint32_t>(eval_smem);
+    if (eval_smem + staged_plan.stage_bytes[4] <= 48 * 1024) {  // keeps four CTAs per SM
+      eval_smem += staged_plan.stage_bytes[4];
+      ctrl_eval_fn = var->ctrl_eval_tmem_staged;
+    }
+  }
   // least squares: the column being orthogonalised in shared memory, or (PP200_LSQ_TMEM=1, n*4L <= 128)
   // in tensor memory with 256-thread CTAs, two per SM (256 TMEM columns each), leaving L1 to Q
   bool lsq_tm = env_size("PP200_LSQ_TMEM", 0) != 0 && static_cast<size_t>(n) * 4 * L <= 128 && tblock == 128;
@@ -593,7 +612,7 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   Carver cv{static_cast<char*>(cx.workspace(bytes))};
 
   dev::TrackArgs a{};
-  a.plan = plan_args(plan, dp);
+  a.plan = staged_plan;
   a.total_degree = st.total_degree ? 1 : 0;
   a.rtol = cfg.residual_tol;
   a.utol = cfg.update_tol;

@@ -42,6 +42,11 @@ struct PlanArgs {
   int n_polys;
   int n_terms;
   int n_slots;               // contribution slots of one evaluation
+  // staging of the tables in shared memory (ctrl_eval_trip<..., kStage>): bytes of term_info,
+  // pos, base, coeff, each a multiple of 16, and their total; the tables start at stage_offset
+  // bytes into the dynamic shared memory
+  uint32_t stage_bytes[5];
+  uint32_t stage_offset;
 };
 
 // One persistent launch of the path tracker.
@@ -146,6 +151,7 @@ struct Variant {
   const void* lsq_qcache;      // lsq_trip with q_i cached in tensor memory between dot and axpy
   const void* lsq_qcache_fuse; // the same with each axpy fused into the next dot product's row loop
   const void* newton;          // __global__ void(NewtonArgs): the corrector alone (set_prediction tests)
+  const void* ctrl_eval_tmem_staged;  // ctrl_eval_tmem with the plan tables staged in shared memory by TMA
 };
 
 // tail compaction: move the busy slots of [keep, n_active) into idle slots of [0, keep)

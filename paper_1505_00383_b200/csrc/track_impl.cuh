@@ -136,15 +136,26 @@ struct Tiled {
   }
 };
 
+// load of a plan-table entry: through the read-only path from global memory, or (kSm) a plain
+// load from the copy the kernel staged in shared memory
+template <bool kSm, class T>
+__device__ __forceinline__ T tld(const T* p) {
+  if constexpr (kSm) {
+    return *p;
+  } else {
+    return __ldg(p);
+  }
+}
+
 // uniform (warp-broadcast) load of a complex table entry stored as 2L consecutive doubles
-template <class R>
+template <class R, bool kSm = false>
 __device__ __forceinline__ cx<R> ld_table(const double* p) {
   constexpr int L = level<R>::L;
   cx<R> z;
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    level<R>::set(z.re, l, __ldg(p + l));
-    level<R>::set(z.im, l, __ldg(p + L + l));
+    level<R>::set(z.re, l, tld<kSm>(p + l));
+    level<R>::set(z.im, l, tld<kSm>(p + L + l));
   }
   return z;
 }
@@ -177,18 +188,18 @@ __device__ __forceinline__ cx<R> ld_flat(const double* p) {
 // variable to dH_poly/dx_var, in the reference's order; jac_pre(var) is called before w is
 // computed.  The Speelpenning prefix stack is a
 // dynamically indexed array (local memory, L1-resident), so the code stays compact for any KMAX.
-template <class R, int KMAX, class SysF, class JacF, class PreF>
+template <class R, int KMAX, bool kSm = false, class SysF, class JacF, class PreF>
 __device__ __forceinline__ void eval_term(const PlanArgs& pa, int i, const Planar<R>& X, size_t xs, const R& t,
                                           const R& u, int& poly_out, SysF&& sys_add, JacF&& jac_add,
                                           PreF&& jac_pre) {
   constexpr int L = level<R>::L;
-  const int4 ti = __ldg(reinterpret_cast<const int4*>(pa.term_info) + i);
+  const int4 ti = tld<kSm>(reinterpret_cast<const int4*>(pa.term_info) + i);
   const int k = ti.y, po = ti.z, nb = ti.w & 0xff, bo = ti.w >> 8;
   poly_out = ti.x;
 
   // coefficient stage: c = c_start*(1-t) + c_target*t (evaldiff.cpp:259-274)
   const double* cp = pa.coeff + static_cast<size_t>(i) * 4 * L;
-  const cx<R> cs = ld_table<R>(cp), ct = ld_table<R>(cp + 2 * L);
+  const cx<R> cs = ld_table<R, kSm>(cp), ct = ld_table<R, kSm>(cp + 2 * L);
   const cx<R> c{radd(rmul(cs.re, u), rmul(ct.re, t)), radd(rmul(cs.im, u), rmul(ct.im, t))};
 
   if (k == 0) {  // constants skip the monomial stage (evaldiff.cpp:345-352)
@@ -201,7 +212,7 @@ __device__ __forceinline__ void eval_term(const PlanArgs& pa, int i, const Plana
   if (nb > 0) {
     bool init = false;
     for (int b = 0; b < nb; ++b) {
-      const uint32_t be = __ldg(pa.base + bo + b);
+      const uint32_t be = tld<kSm>(pa.base + bo + b);
       const cx<R> xv = X.ld(static_cast<int>(be & 0xffffu), xs);
       const uint32_t e = be >> 16;
       if (e == 1) {
@@ -224,7 +235,7 @@ __device__ __forceinline__ void eval_term(const PlanArgs& pa, int i, const Plana
   const uint32_t* pv = pa.pos + po;
   // derivative contribution w = c*d (scaled by the exponent when e != 1) of variable j
   auto contribute = [&](int j, cx<R> d) {
-    const uint32_t pe = __ldg(pv + j);
+    const uint32_t pe = tld<kSm>(pv + j);
     jac_pre(static_cast<int>(pe & 0xffffu));  // lets the accumulator fetch its old value early
     if (nb > 0) d = cmul(d, aux);
     cx<R> w = cmul(c, d);
@@ -234,7 +245,7 @@ __device__ __forceinline__ void eval_term(const PlanArgs& pa, int i, const Plana
   };
 
   if (k == 1) {
-    cx<R> val = X.ld(static_cast<int>(__ldg(pv) & 0xffffu), xs);
+    cx<R> val = X.ld(static_cast<int>(tld<kSm>(pv) & 0xffffu), xs);
     if (nb > 0) val = cmul(val, aux);
     sys_add(cmul(c, val));
     contribute(0, cone<R>());
@@ -244,13 +255,13 @@ __device__ __forceinline__ void eval_term(const PlanArgs& pa, int i, const Plana
   // Speelpenning products (evaldiff.cpp:90-115): prefix P_j = x_p0 ... x_p(j-1) for j < k,
   // value = P_(k-1) x_p(k-1), d_j = P_j * S_(j+1) with the running suffix S.
   cx<R> P[KMAX > 1 ? KMAX : 2];
-  cx<R> run = X.ld(static_cast<int>(__ldg(pv) & 0xffffu), xs);
+  cx<R> run = X.ld(static_cast<int>(tld<kSm>(pv) & 0xffffu), xs);
   P[1] = run;
   for (int j = 2; j < k; ++j) {
-    run = cmul(run, X.ld(static_cast<int>(__ldg(pv + j - 1) & 0xffffu), xs));
+    run = cmul(run, X.ld(static_cast<int>(tld<kSm>(pv + j - 1) & 0xffffu), xs));
     P[j] = run;
   }
-  const cx<R> xlast = X.ld(static_cast<int>(__ldg(pv + k - 1) & 0xffffu), xs);
+  const cx<R> xlast = X.ld(static_cast<int>(tld<kSm>(pv + k - 1) & 0xffffu), xs);
   cx<R> val = cmul(run, xlast);
   if (nb > 0) val = cmul(val, aux);
   sys_add(cmul(c, val));
@@ -258,7 +269,7 @@ __device__ __forceinline__ void eval_term(const PlanArgs& pa, int i, const Plana
   cx<R> acc = xlast;
   for (int j = k - 2; j >= 1; --j) {
     const cx<R> d = cmul(P[j], acc);
-    acc = cmul(acc, X.ld(static_cast<int>(__ldg(pv + j) & 0xffffu), xs));
+    acc = cmul(acc, X.ld(static_cast<int>(tld<kSm>(pv + j) & 0xffffu), xs));
     contribute(j, d);
   }
   contribute(0, acc);  // d_0 = S_1
@@ -438,7 +449,7 @@ struct TmemRow {
 // resid_r = max_p |H_p| at level R (tracker.cpp:488-494).  The coefficient, monomial and sum
 // stages of the reference are fused per term; because the plan is polynomial-major
 // (evaldiff.cpp:200-236), only one row of H/J is open at a time.
-template <class R, int KMAX, class GA, class ROW>
+template <class R, int KMAX, bool kSm = false, class GA, class ROW>
 __device__ void eval_hj(const PlanArgs& pa, const Planar<R>& X, const ROW& JR, size_t ls,
                         const R& t, const GA& B, const GA& J, size_t gs,
                         double& resid_d, R& resid_r) {
@@ -466,11 +477,11 @@ __device__ void eval_hj(const PlanArgs& pa, const Planar<R>& X, const ROW& JR, s
 
   for (int i = 0; i < pa.n_terms; ++i) {
     // terms are polynomial-major: close the rows of the polynomials before this term's
-    const int poly = __ldg(pa.term_info + 4 * i);
+    const int poly = tld<kSm>(pa.term_info + 4 * i);
     while (cur < poly) flush(cur++);
     int p_unused;
     typename ROW::Pending pend;
-    eval_term<R, KMAX>(
+    eval_term<R, KMAX, kSm>(
         pa, i, X, ls, t, u, p_unused, [&](const cx<R>& v) { sacc = cadd(sacc, v); },
         [&](int, int var, const cx<R>& w) { JR.finish_add(var, pend, w); }, [&](int var) { JR.issue(var, pend); });
   }
@@ -1274,10 +1285,45 @@ __global__ void __launch_bounds__(128) step_trip(const TrackArgs a, unsigned* bu
 // it is written back for the least-squares kernel.  The control part counts the slots with work
 // in this trip (busy_out) and the evaluations / solves issued (a.work).
 // ---------------------------------------------------------------------------------------------
-template <class R, int KMAX, bool kTmem, int kMinBlocks>
+// kStage: the plan tables (term info, positions, base factors, coefficients) are copied into
+// shared memory by one bulk TMA transfer each (cp.async.bulk, completion on an mbarrier) when the
+// CTA starts, and the evaluation reads them from there (PlanArgs::stage_* give the layout)
+template <class R, int KMAX, bool kTmem, int kMinBlocks, bool kStage = false>
 __global__ void __launch_bounds__(128, kMinBlocks) ctrl_eval_trip(const TrackArgs a, unsigned* busy_out) {
   constexpr int L = level<R>::L;
   extern __shared__ double smem[];
+  PlanArgs pa_s = a.plan;
+  if constexpr (kStage) {
+    __shared__ __align__(8) unsigned long long mbar;
+    char* tab = reinterpret_cast<char*>(smem) + a.plan.stage_offset;
+    const uint32_t mb = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar));
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb));
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(a.plan.stage_bytes[4])
+                   : "memory");
+      const void* src[4] = {a.plan.term_info, a.plan.pos, a.plan.base, a.plan.coeff};
+      uint32_t off = 0;
+      for (int q = 0; q < 4; ++q) {
+        if (a.plan.stage_bytes[q] != 0)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                           static_cast<uint32_t>(__cvta_generic_to_shared(tab + off))),
+                       "l"(src[q]), "r"(a.plan.stage_bytes[q]), "r"(mb)
+                       : "memory");
+        off += a.plan.stage_bytes[q];
+      }
+    }
+    __syncthreads();
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.b32 %0, 1, 0, p;\n}\n"
+                   : "=r"(done) : "r"(mb) : "memory");
+    pa_s.term_info = reinterpret_cast<const int32_t*>(tab);
+    pa_s.pos = reinterpret_cast<const uint32_t*>(tab + a.plan.stage_bytes[0]);
+    pa_s.base = reinterpret_cast<const uint32_t*>(tab + a.plan.stage_bytes[0] + a.plan.stage_bytes[1]);
+    pa_s.coeff = reinterpret_cast<const double*>(tab + a.plan.stage_bytes[0] + a.plan.stage_bytes[1] +
+                                                 a.plan.stage_bytes[2]);
+  }
   const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const bool in_range = s < a.n_active;
   const int n = a.plan.n;
@@ -1329,11 +1375,11 @@ __global__ void __launch_bounds__(128, kMinBlocks) ctrl_eval_trip(const TrackArg
     // warp-collective TMEM accesses: the warp evaluates if any lane needs it; the other lanes
     // run the same plan on their (unused) point and discard the results
     if (__any_sync(0xffffffffu, need)) {
-      eval_hj<R, KMAX>(a.plan, XS, TmemRow<R>{row_base}, ls, t, B, J, s, resid, resid_r);
+      eval_hj<R, KMAX, kStage>(pa_s, XS, TmemRow<R>{row_base}, ls, t, B, J, s, resid, resid_r);
     }
   } else if (need) {
     const Planar<R> JR{smem + static_cast<size_t>(n) * 2 * L * blockDim.x, blockDim.x};
-    eval_hj<R, KMAX>(a.plan, XS, SmemRow<R>{JR, ls}, ls, t, B, J, s, resid, resid_r);
+    eval_hj<R, KMAX, kStage>(pa_s, XS, SmemRow<R>{JR, ls}, ls, t, B, J, s, resid, resid_r);
   }
   if (need) {
     const Planar<R> X{a.x, a.S}, SR{a.sr, a.S};
@@ -1741,7 +1787,8 @@ __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
    reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, true, 256, 2>),                                        \
    reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, false, 128, PP_LSQ_MINB, true>),                        \
    reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, false, 128, PP_LSQ_MINB, true, true>),                  \
-   reinterpret_cast<const void*>(&pp::dev::newton_kernel<R, KM>)}
+   reinterpret_cast<const void*>(&pp::dev::newton_kernel<R, KM>),                                              \
+   reinterpret_cast<const void*>(&pp::dev::ctrl_eval_trip<R, KM, true, (sizeof(R) < 32 ? 4 : 1), true>)}
 
 // register-resident least-squares solvers of one level for dimension N
 #define PP_LSQ_REG(R, N)                                                                        \

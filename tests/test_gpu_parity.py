@@ -112,7 +112,8 @@ def test_track_bitwise(pp, name, system):
     ("katsura12_qd_mn4", "katsura12"), ("rand32_dd", "rand32"), ("cyclic8_d", "cyclic8"),
 ])
 @pytest.mark.parametrize("mode", ["warp_per_path", "group8_per_path", "group4_per_path", "thread_per_path",
-                                  "thread_per_path_tmem", "thread_per_path_plain", "thread_per_path_fuse"])
+                                  "thread_per_path_tmem", "thread_per_path_plain", "thread_per_path_fuse",
+                                  "thread_per_path_staged"])
 def test_track_bitwise_modes(pp, monkeypatch, name, system, mode):
     """every engine gives the reference records: every trip in tail mode (a warp per path, or 8
     or 4 lanes per path: eval_coop / lsq_coop), or never (a thread per path; small runs otherwise
@@ -130,6 +131,9 @@ def test_track_bitwise_modes(pp, monkeypatch, name, system, mode):
         monkeypatch.setenv("PP200_LSQ_QCACHE", "0")
         monkeypatch.setenv("PP200_LSQ_REG", "0")
     monkeypatch.setenv("PP200_LSQ_FUSE", "1" if mode.endswith("fuse") else "0")
+    if mode.endswith("staged"):  # plan tables staged in shared memory by TMA bulk copies
+        monkeypatch.setenv("PP200_STAGE_TABLES", "1")
+        monkeypatch.setenv("PP200_TMEM", "1")
     if mode.endswith("tmem"):
         monkeypatch.setenv("PP200_TMEM", "1")
         monkeypatch.setenv("PP200_LSQ_TMEM", "1")
