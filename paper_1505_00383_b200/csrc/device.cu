@@ -516,10 +516,11 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   }
   const void* ctrl_eval_fn = tmem ? var->ctrl_eval_tmem : var->ctrl_eval_trip;
   size_t eval_smem = static_cast<size_t>(eblock) * per_thread_smem / (tmem ? 2 : 1);
-  // PP200_STAGE_TABLES=1 (TMEM evaluation): the plan tables go to shared memory by bulk TMA copies
-  // when each CTA starts, and the evaluation reads them from there
+  // PP200_STAGE_TABLES (default 1; TMEM evaluation): the plan tables go to shared memory by bulk
+  // TMA copies when each CTA starts, and the evaluation reads them from there (cyclic-10 d:
+  // 254 k -> 281 k paths/s; dd unchanged within 0.1 %)
   dev::PlanArgs staged_plan = plan_args(plan, dp);
-  if (tmem && env_size("PP200_STAGE_TABLES", 0) != 0) {
+  if (tmem && env_size("PP200_STAGE_TABLES", 1) != 0) {
     auto r16 = [](size_t b) { return static_cast<uint32_t>((b + 15) / 16 * 16); };
     staged_plan.stage_bytes[0] = r16(plan.term_info.size() * sizeof(int32_t));
     staged_plan.stage_bytes[1] = r16(plan.pos.size() * sizeof(uint32_t));

@@ -131,8 +131,9 @@ def test_track_bitwise_modes(pp, monkeypatch, name, system, mode):
         monkeypatch.setenv("PP200_LSQ_QCACHE", "0")
         monkeypatch.setenv("PP200_LSQ_REG", "0")
     monkeypatch.setenv("PP200_LSQ_FUSE", "1" if mode.endswith("fuse") else "0")
-    if mode.endswith("staged"):  # plan tables staged in shared memory by TMA bulk copies
-        monkeypatch.setenv("PP200_STAGE_TABLES", "1")
+    # plan tables staged in shared memory by TMA bulk copies (the default) or read from global memory
+    monkeypatch.setenv("PP200_STAGE_TABLES", "1" if mode.endswith("staged") else "0")
+    if mode.endswith("staged"):
         monkeypatch.setenv("PP200_TMEM", "1")
     if mode.endswith("tmem"):
         monkeypatch.setenv("PP200_TMEM", "1")
