@@ -326,7 +326,7 @@ void device_init(int device) {
       for (const void* k : {v[i].ctrl_eval_trip, v[i].lsq_trip, v[i].step_trip, v[i].eval, v[i].lsq, v[i].eval_coop[0],
                             v[i].eval_coop[1], v[i].eval_coop[2], v[i].lsq_coop[0], v[i].lsq_coop[1], v[i].lsq_coop[2],
                             v[i].lsq_coop_g[0], v[i].lsq_coop_g[1], v[i].lsq_coop_g[2], v[i].ctrl_eval_tmem,
-                            v[i].lsq_qcache, v[i].lsq_qcache_fuse, v[i].ctrl_eval_tmem_staged, v[i].lsq_pair}) {
+                            v[i].lsq_qcache, v[i].lsq_qcache_fuse, v[i].ctrl_eval_tmem_staged}) {
         cudaFuncAttributes at;
         check(cudaFuncGetAttributes(&at, k), "kernel load");
       }
@@ -758,15 +758,6 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
       while (gi > 0 && coop_wpb(ecoop_slot, gi) < 1) --gi;
       return gi;
     };
-    // thread mode with few busy slots: the solver runs with two lanes per slot (lsq_coop<R, true, 2>:
-    // rows split over the pair, the reference's sums on both lanes), which doubles the solver's
-    // warps while the evaluation stays a thread per slot.  From PP200_PAIR_SLOTS (128 per SM) busy
-    // slots down to the tail-mode threshold.
-    const size_t pair_slot = static_cast<size_t>(4) * n * el;
-    const int pair_wpb = static_cast<int>(std::min<size_t>(4, (200 * 1024) / (pair_slot * 16)));
-    const size_t pair_slots = env_size("PP200_PAIR_SLOTS", 128 * static_cast<size_t>(prop.multiProcessorCount));
-    const bool pair_ok = pair_wpb >= 1 && var->lsq_pair != nullptr && pair_slots > 0;
-    if (pair_ok) ensure_smem(var->lsq_pair, pair_wpb * 16 * pair_slot, device);
     // tail mode needs a warp per slot to fit (G = 32)
     const bool coop_ok = coop_wpb(ecoop_slot, 0) >= 1 && coop_wpb(lcoop_slot, 0) >= 1;
     for (int gi = 0; gi < 3 && coop_ok; ++gi) {
@@ -815,17 +806,10 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
         check(cudaLaunchKernel(ctrl_eval_fn, egrid(), dim3(eblock), args, eval_smem, stream),
               "launch ctrl_eval_trip");
         if (ev) check(cudaEventRecord(ev[2], stream), "event");
-        if (pair_ok && a.n_active <= pair_slots) {
-          const size_t per_block = static_cast<size_t>(pair_wpb) * 16;
-          check(cudaLaunchKernel(var->lsq_pair, dim3(static_cast<unsigned>((a.n_active + per_block - 1) / per_block)),
-                                 dim3(32 * pair_wpb), targs, per_block * pair_slot, stream),
-                "launch lsq_coop (pairs)");
-        } else {
-          const size_t per_block = static_cast<size_t>(lblock) * a.lsq_spt;
-          check(cudaLaunchKernel(lsq_fn, dim3(static_cast<unsigned>((a.n_active + per_block - 1) / per_block)), dim3(lblock),
-                                 targs, lsq_smem, stream),
-                "launch lsq_trip");
-        }
+        const size_t per_block = static_cast<size_t>(lblock) * a.lsq_spt;
+        check(cudaLaunchKernel(lsq_fn, dim3(static_cast<unsigned>((a.n_active + per_block - 1) / per_block)), dim3(lblock),
+                               targs, lsq_smem, stream),
+              "launch lsq_trip");
       }
       if (ev) check(cudaEventRecord(ev[3], stream), "event");
       launches += coop ? 3 : 2;

@@ -152,7 +152,6 @@ struct Variant {
   const void* lsq_qcache_fuse; // the same with each axpy fused into the next dot product's row loop
   const void* newton;          // __global__ void(NewtonArgs): the corrector alone (set_prediction tests)
   const void* ctrl_eval_tmem_staged;  // ctrl_eval_tmem with the plan tables staged in shared memory by TMA
-  const void* lsq_pair;        // lsq_coop with two lanes per slot (global Q), the thread mode's solver when few slots are busy
 };
 
 // tail compaction: move the busy slots of [keep, n_active) into idle slots of [0, keep)
