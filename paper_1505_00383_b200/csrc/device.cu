@@ -326,7 +326,7 @@ void device_init(int device) {
       for (const void* k : {v[i].ctrl_eval_trip, v[i].lsq_trip, v[i].step_trip, v[i].eval, v[i].lsq, v[i].eval_coop[0],
                             v[i].eval_coop[1], v[i].eval_coop[2], v[i].lsq_coop[0], v[i].lsq_coop[1], v[i].lsq_coop[2],
                             v[i].lsq_coop_g[0], v[i].lsq_coop_g[1], v[i].lsq_coop_g[2], v[i].ctrl_eval_tmem,
-                            v[i].lsq_qcache, v[i].lsq_qcache_fuse, v[i].ctrl_eval_tmem_staged}) {
+                            v[i].lsq_qcache, v[i].lsq_qcache_fuse, v[i].ctrl_eval_tmem_staged, v[i].lsq_qcache_fuse_l2}) {
         cudaFuncAttributes at;
         check(cudaFuncGetAttributes(&at, k), "kernel load");
       }
@@ -508,11 +508,12 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   bool tmem = env_size("PP200_TMEM", 1) != 0 && static_cast<size_t>(n) * 4 * L <= 128 && eblock == 128;
   uint32_t tmem_cols = 32;
   while (tmem_cols < static_cast<uint32_t>(n) * 4 * L) tmem_cols *= 2;
+  int eval_ctas = 0;  // resident CTAs per SM of the TMEM evaluation
   if (tmem) {
     // every resident CTA must get its columns at once (512 per SM), or tcgen05.alloc would stall
     ensure_smem(var->ctrl_eval_tmem, eblock * per_thread_smem / 2, device);
-    tmem = static_cast<uint32_t>(occupancy(var->ctrl_eval_tmem, eblock, eblock * per_thread_smem / 2, device)) *
-               tmem_cols <= 512;
+    eval_ctas = occupancy(var->ctrl_eval_tmem, eblock, eblock * per_thread_smem / 2, device);
+    tmem = static_cast<uint32_t>(eval_ctas) * tmem_cols <= 512;
   }
   const void* ctrl_eval_fn = tmem ? var->ctrl_eval_tmem : var->ctrl_eval_trip;
   size_t eval_smem = static_cast<size_t>(eblock) * per_thread_smem / (tmem ? 2 : 1);
@@ -529,7 +530,9 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
     staged_plan.stage_bytes[4] =
         staged_plan.stage_bytes[0] + staged_plan.stage_bytes[1] + staged_plan.stage_bytes[2] + staged_plan.stage_bytes[3];
     staged_plan.stage_offset = static_cast<uint32_t>(eval_smem);
-    if (eval_smem + staged_plan.stage_bytes[4] <= 48 * 1024) {  // keeps four CTAs per SM
+    // only while the tables do not cost a resident CTA (1 KB per CTA is reserved by the runtime)
+    if ((eval_smem + staged_plan.stage_bytes[4] + 1024) * static_cast<size_t>(eval_ctas) <=
+        prop.sharedMemPerMultiprocessor) {
       eval_smem += staged_plan.stage_bytes[4];
       ctrl_eval_fn = var->ctrl_eval_tmem_staged;
     }
@@ -562,6 +565,8 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   // PP200_LSQ_FUSE (default 1): with the q-cache, each axpy shares its row loop with the next dot
   // product (cyclic-10 dd: lsq 9.73 -> 9.54 s per 262,144 paths; cyclic-8 dd +2.3 %)
   if (lsq_qc) lsq_fn = env_size("PP200_LSQ_FUSE", 1) != 0 ? var->lsq_qcache_fuse : var->lsq_qcache;
+  // PP200_LSQ_L2HINT=1: the fused solver with L2 eviction policies on Q (first half of the columns kept)
+  if (lsq_qc && env_size("PP200_LSQ_FUSE", 1) != 0 && env_size("PP200_LSQ_L2HINT", 0) != 0) lsq_fn = var->lsq_qcache_fuse_l2;
   const int lblock = lsq_tm ? 256 : tblock;
   size_t lsq_smem = (lsq_tm || lsq_reg) ? 0 : static_cast<size_t>(tblock) * per_thread_smem / 2;
   if (lsq_qc) lsq_smem = std::max<size_t>(lsq_smem, (prop.sharedMemPerMultiprocessor / 5) + 1024);

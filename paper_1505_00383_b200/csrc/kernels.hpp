@@ -152,6 +152,7 @@ struct Variant {
   const void* lsq_qcache_fuse; // the same with each axpy fused into the next dot product's row loop
   const void* newton;          // __global__ void(NewtonArgs): the corrector alone (set_prediction tests)
   const void* ctrl_eval_tmem_staged;  // ctrl_eval_tmem with the plan tables staged in shared memory by TMA
+  const void* lsq_qcache_fuse_l2;     // lsq_qcache_fuse with L2 evict_last / evict_first policies on Q
 };
 
 // tail compaction: move the busy slots of [keep, n_active) into idle slots of [0, keep)

@@ -134,7 +134,43 @@ struct Tiled {
       p[(L + l) * 32] = level<R>::get(z.im, l);
     }
   }
+  // the same with an L2 cache policy (createpolicy: evict_last keeps the line, evict_first lets it go)
+  __device__ __forceinline__ cx<R> ldp(int e, size_t s, uint64_t pol) const {
+    cx<R> z;
+    const double* p = at(e, s);
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      double a, b;
+      asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(a) : "l"(p + l * 32), "l"(pol));
+      asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(b) : "l"(p + (L + l) * 32), "l"(pol));
+      level<R>::set(z.re, l, a);
+      level<R>::set(z.im, l, b);
+    }
+    return z;
+  }
+  __device__ __forceinline__ void stp(int e, size_t s, const cx<R>& z, uint64_t pol) const {
+    double* p = at(e, s);
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p + l * 32), "d"(level<R>::get(z.re, l)), "l"(pol)
+                   : "memory");
+      asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p + (L + l) * 32), "d"(level<R>::get(z.im, l)),
+                   "l"(pol)
+                   : "memory");
+    }
+  }
 };
+
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 
 // load of a plan-table entry: through the read-only path from global memory, or (kSm) a plain
 // load from the copy the kernel staged in shared memory
@@ -590,9 +626,32 @@ struct TmemQCache {
 // rows fill the latency of the sequential sum.  Every operation and every sum order is the
 // reference's: the dot product of projection j+1 reads each row after projection j's axpy has
 // updated it, exactly as the two separate loops do.
-template <class R, class GA, class CA, bool kUniform, class QC = NoQCache, bool kFuse = false>
+// kHint (slot-tiled Q, fused path): the first half of the columns -- read most often, q_i by all
+// later columns in both passes -- are loaded and stored with an L2 evict_last policy, the rest
+// with evict_first, so that the most reused columns of all slots stay in L2
+template <class R, class GA, class CA, bool kUniform, class QC = NoQCache, bool kFuse = false, bool kHint = false>
 __device__ bool lsq_solve_c(int n, int m, double rank_tol, const GA& Q, const GA& Rm, const GA& B, const GA& Y,
                             size_t s, const CA& C, const QC& qc = QC{}) {
+  [[maybe_unused]] uint64_t pol_keep = 0, pol_drop = 0;
+  if constexpr (kHint) {
+    pol_keep = l2_policy_evict_last();
+    pol_drop = l2_policy_evict_first();
+  }
+  const int keep_cols = (n + 1) / 2;
+  auto qld = [&](int col, int row) -> cx<R> {
+    if constexpr (kHint) {
+      return Q.ldp(col * m + row, s, col < keep_cols ? pol_keep : pol_drop);
+    } else {
+      return Q.ld(col * m + row, s);
+    }
+  };
+  auto qst = [&](int col, int row, const cx<R>& z) {
+    if constexpr (kHint) {
+      Q.stp(col * m + row, s, z, col < keep_cols ? pol_keep : pol_drop);
+    } else {
+      Q.st(col * m + row, s, z);
+    }
+  };
   // m x n (m >= n rows; the tracker's systems are square, m == n): Q column-major, element col*m + row
   const cx<R> zero = czero<R>();
   R max_norm = rfrom<R>(0.0);
@@ -610,14 +669,14 @@ PP_UNROLL_ROWS
   bool ok = true;
   for (int k = 0; k < n; ++k) {
 PP_UNROLL_ROWS
-    for (int r = 0; r < m; ++r) C.st(r, Q.ld(k * m + r, s));
+    for (int r = 0; r < m; ++r) C.st(r, qld(k, r));
     const int rk = k * (k + 1) / 2;
     if (kFuse && k > 0) {
       // the 2k projections of column k in order: pass 0 on q_0 .. q_(k-1), then pass 1
       cx<R> rik = zero;
 PP_UNROLL_ROWS
       for (int r = 0; r < m; ++r) {
-        const cx<R> q = Q.ld(r, s);  // q_0
+        const cx<R> q = qld(0, r);  // q_0
         qc.put(r, q);
         rik = cadd(rik, cmul(cconj(q), C.ld(r)));
       }
@@ -633,7 +692,7 @@ PP_UNROLL_ROWS
           for (int r = 0; r < m; ++r) {
             const cx<R> qi = qc.template get<R>(r, Q, i * m + r, s);
             const cx<R> c = csub(C.ld(r), cmul(rik, qi));  // axpy of projection j
-            const cx<R> qn = Q.ld(in * m + r, s);
+            const cx<R> qn = qld(in, r);
             qc.put(r, qn);
             C.st(r, c);
             rnext = cadd(rnext, cmul(cconj(qn), c));  // dot product of projection j + 1
@@ -678,7 +737,7 @@ PP_UNROLL_ROWS
 PP_UNROLL_ROWS
     for (int r = 0; r < m; ++r) {
       const cx<R> q = cmulr(C.ld(r), rinv);
-      Q.st(k * m + r, s, q);
+      qst(k, r, q);
       y = cadd(y, cmul(cconj(q), B.ld(r, s)));  // y_k = <q_k, b> (linalg.hpp:117)
     }
     Y.st(k, s, y);
@@ -741,7 +800,8 @@ __device__ __forceinline__ void tmem_free_cta(uint32_t base) {
 // product).  Its accesses are warp-collective, so a warp runs the solve if any lane needs it.
 // kQCache (with kTmem false): the column in shared memory, and each projected q_i cached in the
 // thread's TMEM lane between its dot product and its axpy (TmemQCache); warp-collective as well.
-template <class R, bool kTmem, int kThreads, int kMinBlocks, bool kQCache = false, bool kFuse = false>
+template <class R, bool kTmem, int kThreads, int kMinBlocks, bool kQCache = false, bool kFuse = false,
+          bool kHint = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) lsq_trip(const TrackArgs a) {
   constexpr int L = level<R>::L;
   extern __shared__ double smem[];
@@ -770,7 +830,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) lsq_trip(const TrackArgs
       if (!__any_sync(0xffffffffu, need_r)) continue;
       const size_t so = in_r ? sr : s;  // out-of-range lanes run on their first slot's scratch
       const bool ok =
-          lsq_solve_c<R, decltype(J), SmemRow<R>, true, TmemQCache<R>, kFuse>(n, n, a.rank_tol, J, Rm, B, Y, so, C, qc);
+          lsq_solve_c<R, decltype(J), SmemRow<R>, true, TmemQCache<R>, kFuse, kHint>(n, n, a.rank_tol, J, Rm, B, Y, so,
+                                                                                      C, qc);
       if (need_r) si(F_OK, sr) = ok ? 1 : 0;
       if (need_r && ok) {
         double dxn = 0.0, xn = 0.0;
@@ -1788,7 +1849,8 @@ __global__ void __launch_bounds__(128) lsq_kernel(const LsqArgs a) {
    reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, false, 128, PP_LSQ_MINB, true>),                        \
    reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, false, 128, PP_LSQ_MINB, true, true>),                  \
    reinterpret_cast<const void*>(&pp::dev::newton_kernel<R, KM>),                                              \
-   reinterpret_cast<const void*>(&pp::dev::ctrl_eval_trip<R, KM, true, (sizeof(R) < 32 ? 4 : 1), true>)}
+   reinterpret_cast<const void*>(&pp::dev::ctrl_eval_trip<R, KM, true, (sizeof(R) < 32 ? 4 : 1), true>),          \
+   reinterpret_cast<const void*>(&pp::dev::lsq_trip<R, false, 128, PP_LSQ_MINB, true, true, true>)}
 
 // register-resident least-squares solvers of one level for dimension N
 #define PP_LSQ_REG(R, N)                                                                        \

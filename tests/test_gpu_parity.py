@@ -113,7 +113,7 @@ def test_track_bitwise(pp, name, system):
 ])
 @pytest.mark.parametrize("mode", ["warp_per_path", "group8_per_path", "group4_per_path", "thread_per_path",
                                   "thread_per_path_tmem", "thread_per_path_plain", "thread_per_path_fuse",
-                                  "thread_per_path_staged"])
+                                  "thread_per_path_staged", "thread_per_path_l2hint"])
 def test_track_bitwise_modes(pp, monkeypatch, name, system, mode):
     """every engine gives the reference records: every trip in tail mode (a warp per path, or 8
     or 4 lanes per path: eval_coop / lsq_coop), or never (a thread per path; small runs otherwise
@@ -131,6 +131,7 @@ def test_track_bitwise_modes(pp, monkeypatch, name, system, mode):
         monkeypatch.setenv("PP200_LSQ_QCACHE", "0")
         monkeypatch.setenv("PP200_LSQ_REG", "0")
     monkeypatch.setenv("PP200_LSQ_FUSE", "1" if mode.endswith("fuse") else "0")
+    monkeypatch.setenv("PP200_LSQ_L2HINT", "1" if mode.endswith("l2hint") else "0")
     # plan tables staged in shared memory by TMA bulk copies (the default) or read from global memory
     monkeypatch.setenv("PP200_STAGE_TABLES", "1" if mode.endswith("staged") else "0")
     if mode.endswith("staged"):
