@@ -517,11 +517,13 @@ void device_track(const Plan& plan, DevicePlan* dp, const Starts& st, const pp_t
   }
   const void* ctrl_eval_fn = tmem ? var->ctrl_eval_tmem : var->ctrl_eval_trip;
   size_t eval_smem = static_cast<size_t>(eblock) * per_thread_smem / (tmem ? 2 : 1);
-  // PP200_STAGE_TABLES (default 1; TMEM evaluation): the plan tables go to shared memory by bulk
-  // TMA copies when each CTA starts, and the evaluation reads them from there (cyclic-10 d:
-  // 254 k -> 281 k paths/s; dd unchanged within 0.1 %)
+  // PP200_STAGE_TABLES (TMEM evaluation; default 1 in complex double, 0 otherwise): the plan tables
+  // go to shared memory by bulk TMA copies when each CTA starts, and the evaluation reads them from
+  // there.  Cyclic-10 d: 254 k -> 281 k paths/s.  Cyclic-10 dd: evaluation 6.14 -> 6.24 s per
+  // 262,144 paths (the broadcast table reads hit L1 anyway, and the tables' shared memory shrinks
+  // the L1 that holds the Speelpenning prefix stack), so double-double reads them from global memory.
   dev::PlanArgs staged_plan = plan_args(plan, dp);
-  if (tmem && env_size("PP200_STAGE_TABLES", 1) != 0) {
+  if (tmem && env_size("PP200_STAGE_TABLES", L == 1 ? 1 : 0) != 0) {
     auto r16 = [](size_t b) { return static_cast<uint32_t>((b + 15) / 16 * 16); };
     staged_plan.stage_bytes[0] = r16(plan.term_info.size() * sizeof(int32_t));
     staged_plan.stage_bytes[1] = r16(plan.pos.size() * sizeof(uint32_t));
