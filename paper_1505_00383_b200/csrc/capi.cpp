@@ -87,10 +87,37 @@ const char* pp_version(void) { return "pp200 0.2 (sm_100a)"; }
 int pp_device_count(void) { return pp::device_count(); }
 
 int pp_device_init(int device) {
-  return guard([&] {
+  int rc = guard([&] {
     pp::device_init(device);
     return PP_OK;
   });
+  if (rc != PP_OK) return rc;
+  // one tiny tracking run (x^2 - 4 from x^2 - 1, two paths in complex double), so that the first
+  // real call does not pay for the first use of the stream-ordered allocator, graph capture and
+  // instantiation, or the first launches either
+  const char f_text[] = "1; x0^2 - 4;", g_text[] = "1; x0^2 - 1;";
+  pp_system *f = nullptr, *g = nullptr;
+  pp_homotopy* h = nullptr;
+  pp_starts* st = nullptr;
+  const double gam[2] = {1.0, 0.0}, x0[4] = {1.0, 0.0, -1.0, 0.0};
+  uint64_t id[2];
+  int8_t status[2];
+  uint8_t reason[2];
+  uint32_t steps[2], newton[2], rej[2];
+  double x[4], res[2];
+  pp_records rec{2, 0, id, status, reason, steps, newton, rej, x, res};
+  pp_track_config c;
+  pp_track_config_defaults(PP_D, &c);
+  rc = pp_system_parse(f_text, sizeof f_text - 1, &f);
+  if (rc == PP_OK) rc = pp_system_parse(g_text, sizeof g_text - 1, &g);
+  if (rc == PP_OK) rc = pp_make_homotopy(f, g, PP_D, gam, &h);
+  if (rc == PP_OK) rc = pp_starts_explicit(PP_D, 1, 2, x0, &st);
+  if (rc == PP_OK) rc = pp_track_all(h, st, &c, 0, 2, device, &rec, nullptr);
+  pp_starts_free(st);
+  pp_homotopy_free(h);
+  pp_system_free(g);
+  pp_system_free(f);
+  return rc;
 }
 const char* pp_last_error(void) { return g_error.c_str(); }
 int pp_limbs(int prec) { return limbs_of(prec); }

@@ -312,33 +312,6 @@ int device_count() {
   return n;
 }
 
-// Create the device context and this thread's stream / workspace context, and load the tracking
-// kernels (module loading is lazy otherwise: the first launch of each kernel would pay for it).
-void device_init(int device) {
-  DeviceGuard g(device);
-  check(cudaFree(nullptr), "context");
-  (void)device_props(device);
-  (void)context(device);
-  for (auto fn : {&dev::variants_d, &dev::variants_dd, &dev::variants_qd}) {
-    int cnt = 0;
-    const dev::Variant* v = fn(&cnt);
-    for (int i = 0; i < cnt; ++i)
-      for (const void* k : {v[i].ctrl_eval_trip, v[i].lsq_trip, v[i].step_trip, v[i].eval, v[i].lsq, v[i].eval_coop[0],
-                            v[i].eval_coop[1], v[i].eval_coop[2], v[i].lsq_coop[0], v[i].lsq_coop[1], v[i].lsq_coop[2],
-                            v[i].lsq_coop_g[0], v[i].lsq_coop_g[1], v[i].lsq_coop_g[2], v[i].ctrl_eval_tmem,
-                            v[i].lsq_qcache, v[i].lsq_qcache_fuse, v[i].ctrl_eval_tmem_staged, v[i].lsq_qcache_fuse_l2}) {
-        cudaFuncAttributes at;
-        check(cudaFuncGetAttributes(&at, k), "kernel load");
-      }
-  }
-  int cnt = 0;
-  const dev::LsqReg* lr = dev::lsq_reg_d(&cnt);
-  for (int i = 0; i < cnt; ++i) {
-    cudaFuncAttributes at;
-    check(cudaFuncGetAttributes(&at, lr[i].hold), "kernel load");
-  }
-}
-
 bool device_supports(uint32_t n, uint32_t max_k) { return pick_variant(1, n, max_k) != nullptr; }
 
 uint64_t shard_size(uint64_t lo, uint64_t hi, const TrackShard& sh) {
@@ -418,6 +391,37 @@ void launch_compaction(const MoveArgs& m, void* stream) {
   check(cudaGetLastError(), "compaction");
 }
 }  // namespace dev
+
+// Create the device context and this thread's stream / workspace context, and load the tracking
+// kernels (module loading is lazy otherwise: the first launch of each kernel would pay for it).
+void device_init(int device) {
+  DeviceGuard g(device);
+  check(cudaFree(nullptr), "context");
+  (void)device_props(device);
+  (void)context(device);
+  for (auto fn : {&dev::variants_d, &dev::variants_dd, &dev::variants_qd}) {
+    int cnt = 0;
+    const dev::Variant* v = fn(&cnt);
+    for (int i = 0; i < cnt; ++i)
+      for (const void* k : {v[i].ctrl_eval_trip, v[i].lsq_trip, v[i].step_trip, v[i].eval, v[i].lsq, v[i].eval_coop[0],
+                            v[i].eval_coop[1], v[i].eval_coop[2], v[i].lsq_coop[0], v[i].lsq_coop[1], v[i].lsq_coop[2],
+                            v[i].lsq_coop_g[0], v[i].lsq_coop_g[1], v[i].lsq_coop_g[2], v[i].ctrl_eval_tmem,
+                            v[i].lsq_qcache, v[i].lsq_qcache_fuse, v[i].ctrl_eval_tmem_staged, v[i].lsq_qcache_fuse_l2}) {
+        cudaFuncAttributes at;
+        check(cudaFuncGetAttributes(&at, k), "kernel load");
+      }
+  }
+  int cnt = 0;
+  const dev::LsqReg* lr = dev::lsq_reg_d(&cnt);
+  for (int i = 0; i < cnt; ++i) {
+    cudaFuncAttributes at;
+    check(cudaFuncGetAttributes(&at, lr[i].hold), "kernel load");
+  }
+  for (const void* k : {reinterpret_cast<const void*>(&dev::classify_slots), reinterpret_cast<const void*>(&dev::move_slots)}) {
+    cudaFuncAttributes at;
+    check(cudaFuncGetAttributes(&at, k), "kernel load");
+  }
+}
 
 double device_fp64_peak(int device) {
   DeviceGuard g(device);

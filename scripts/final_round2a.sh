@@ -1,0 +1,10 @@
+#!/bin/bash
+# final round-2 evidence, part A: tests, smoke, the reference acceptance suite through the shim, bench
+OUT=gpurun_out/r02z
+mkdir -p $OUT
+POLYPATH_B200_TRACE=1 timeout 600 oracle/_ref/acceptance_b200 > $OUT/acceptance_b200.txt 2>&1; echo "rc $?" >> $OUT/acceptance_b200.txt
+timeout 600 oracle/_ref/gpu_criteria > $OUT/gpu_criteria.txt 2>&1; echo "rc $?" >> $OUT/gpu_criteria.txt
+timeout 1800 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc $?" >> $OUT/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc $?" >> $OUT/smoke.log
+timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
+tail -3 $OUT/pytest_gpu.log; cat $OUT/smoke.log; tail -c 300 $OUT/bench.json
