@@ -9,8 +9,9 @@
 // __ddiv_rn, __dsqrt_rn), which the compiler never contracts or reassociates; on the host the same
 // source is compiled with -ffp-contract=off.  Both round to nearest-even, so both agree with the
 // reference bit for bit.  Quad-double addition merges limbs in a data-dependent order
-// (xprec.hpp:325-382); here the merge is expressed over register queues (no dynamic array
-// indexing, so nothing spills to local memory) while taking the same decisions.
+// (xprec.hpp:325-382); here the merge is a sorting network on the limbs' magnitudes that emits the
+// same sequence whenever the operands' limbs are ordered (every renormalised value), with the
+// step-by-step merge over register queues for any other operand (qdi::add_i).
 #pragma once
 
 #include <cmath>
@@ -338,7 +339,42 @@ PP_HD qd_t rneg(qd_t a) { return qd_t{-a.c0, -a.c1, -a.c2, -a.c3}; }
 
 // accurate merge-based addition (xprec.hpp:325-382)
 namespace qdi {
-PP_QD_INL qd_t add_i(qd_t a, qd_t b) {
+// the accumulation over the merged limbs m0..m7 (the reference's loop after its merge)
+PP_HD qd_t accumulate_merged(double m0, double m1, double m2, double m3, double m4, double m5, double m6,
+                             double m7) {
+  double v0;
+  const double u0 = quick_two_sum(m0, m1, v0);
+  double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0, x4 = 0.0;
+  double u = u0, v = v0;
+  int k = 0;
+  const double m[6] = {m2, m3, m4, m5, m6, m7};
+PP_UNROLL
+  for (int step = 0; step < 6; ++step) {
+    const double t = m[step];
+    if (k < 4) {
+      double s = qdi::three_accum(u, v, t);
+      if (s != 0.0) {
+        qdi::put(x0, x1, x2, x3, k, s);
+        ++k;
+        if (k == 4) x4 = f_add(u, v);
+      }
+    } else {
+      x4 = f_add(x4, t);
+    }
+  }
+  if (k < 4) {
+    qdi::put(x0, x1, x2, x3, k, u);
+    if (k < 3)
+      qdi::put(x0, x1, x2, x3, k + 1, v);
+    else
+      x4 = v;
+  }
+  return qdi::renorm5_i(x0, x1, x2, x3, x4);
+}
+
+// The reference's merge, step by step over two limb queues: correct for any limbs (unsorted,
+// NaN), but on the GPU every step shifts both queues under predicates.
+PP_QD_INL qd_t add_seq_i(qd_t a, qd_t b) {
   qdi::LimbQueue qa{a.c0, a.c1, a.c2, a.c3, 4};
   qdi::LimbQueue qb{b.c0, b.c1, b.c2, b.c3, 4};
   double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0, x4 = 0.0;
@@ -371,6 +407,50 @@ PP_UNROLL
       x4 = v;
   }
   return qdi::renorm5_i(x0, x1, x2, x3, x4);
+}
+}  // namespace qdi
+PP_QD_FN qd_t radd_seq(qd_t a, qd_t b) { return qdi::add_seq_i(a, b); }
+
+namespace qdi {
+// compare-exchange of the merge key: x goes first iff |x| > |y|, or |x| == |y| and x's tag is lower
+PP_HD void merge_cx(double& x, int& tx, double& y, int& ty) {
+  const double ax = f_abs(x), ay = f_abs(y);
+  const bool first = (ax > ay) | ((ax == ay) & (tx < ty));
+  const double lo = first ? y : x;
+  const int tlo = first ? ty : tx;
+  x = first ? x : y;
+  tx = first ? tx : ty;
+  y = lo;
+  ty = tlo;
+}
+
+// The same addition with the merge done by a network.  When both operands' limbs are ordered by
+// non-increasing magnitude (every renormalised value), the reference's merge -- take a_i while
+// |a_i| > |b_j|, else b_j -- emits the limbs in the order of the key (|x| descending; among equal
+// magnitudes b's limbs before a's, each operand's in index order).  Tagging b_j with j and a_i with
+// 4 + i makes that key a total order, so Batcher's odd-even merge of the two sorted runs (9
+// compare-exchanges, 3 levels) yields the identical sequence.  Any other operand (unordered limbs,
+// NaN) takes the step-by-step merge.
+#ifndef PP_QD_ADD_NET
+#define PP_QD_ADD_NET 1
+#endif
+PP_QD_INL qd_t add_i(qd_t a, qd_t b) {
+  if (!PP_QD_ADD_NET) return qdi::add_seq_i(a, b);
+  const bool sorted = (f_abs(a.c0) >= f_abs(a.c1)) & (f_abs(a.c1) >= f_abs(a.c2)) & (f_abs(a.c2) >= f_abs(a.c3)) &
+                      (f_abs(b.c0) >= f_abs(b.c1)) & (f_abs(b.c1) >= f_abs(b.c2)) & (f_abs(b.c2) >= f_abs(b.c3));
+  if (!sorted) return radd_seq(a, b);
+  double w0 = a.c0, w1 = a.c1, w2 = a.c2, w3 = a.c3, w4 = b.c0, w5 = b.c1, w6 = b.c2, w7 = b.c3;
+  int t0 = 4, t1 = 5, t2 = 6, t3 = 7, t4 = 0, t5 = 1, t6 = 2, t7 = 3;
+  merge_cx(w0, t0, w4, t4);
+  merge_cx(w1, t1, w5, t5);
+  merge_cx(w2, t2, w6, t6);
+  merge_cx(w3, t3, w7, t7);
+  merge_cx(w2, t2, w4, t4);
+  merge_cx(w3, t3, w5, t5);
+  merge_cx(w1, t1, w2, t2);
+  merge_cx(w3, t3, w4, t4);
+  merge_cx(w5, t5, w6, t6);
+  return accumulate_merged(w0, w1, w2, w3, w4, w5, w6, w7);
 }
 }  // namespace qdi
 PP_QD_FN qd_t radd(qd_t a, qd_t b) { return qdi::add_i(a, b); }
