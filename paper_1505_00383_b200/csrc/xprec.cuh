@@ -430,7 +430,8 @@ PP_HD void merge_cx(double& x, int& tx, double& y, int& ty) {
 // magnitudes b's limbs before a's, each operand's in index order).  Tagging b_j with j and a_i with
 // 4 + i makes that key a total order, so Batcher's odd-even merge of the two sorted runs (9
 // compare-exchanges, 3 levels) yields the identical sequence.  Any other operand (unordered limbs,
-// NaN) takes the step-by-step merge.
+// NaN) takes the step-by-step merge.  tests/native/qd_add_check.cpp compares the two bit for bit;
+// building with -DPP_QD_ADD_NET=0 uses the step-by-step merge everywhere (A/B).
 #ifndef PP_QD_ADD_NET
 #define PP_QD_ADD_NET 1
 #endif
